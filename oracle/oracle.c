@@ -1,0 +1,211 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct serial CPU oracle for the BFS of arXiv 1408.1605.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load this library.  It shares no code, header, table or helper
+ * with the CUDA path (paper_1408_1605_b200/csrc); it does not know about 2D partitions, CSC
+ * blocks, bitmaps, prefix sums or binary searches.  It takes a plain tuple list.
+ *
+ * What it computes (the definition the method reaches exactly):
+ *   G = undirected simple graph with edge {s_k, d_k} for every tuple k with s_k != d_k
+ *       ("We turn the graph undirected by adding, for each edge, its opposite";
+ *        duplicates collapse, self-loops never matter: SPEC.md S:204).
+ *   level[v]  = hop distance from root r in G, -1 if unreachable
+ *               (Alg.1/Alg.2: level[r] = 0, others -1 until reached at lvl).
+ *   parent[r] = r;  parent[v] = min{ u : {u,v} in E(G), level[u] = level[v]-1 }
+ *               for reachable v != r (the deterministic minimum-id rule of BASELINE.json's
+ *               north_star, reading R1); -1 if unreachable.
+ *   m_comp    = |{ k : level[s_k] >= 0 }|, every input tuple of the traversed component,
+ *               duplicates and self-loops included ("number of input edge tuples
+ *               within the component traversed by the search").
+ *
+ * Algorithm, in the order a reader checks it:
+ *   1. oracle_build: undirected adjacency by counting sort of the 2M tuple endpoints
+ *      (self-loops skipped, duplicates kept -- they do not change distances or the min).
+ *   2. oracle_bfs:   FIFO-queue BFS from r sets level[] (textbook BFS).
+ *   3.               parent pass over the tuple list, both orientations:
+ *                    if level[a] >= 0 and level[b] == level[a]+1 then parent[b] = min(parent[b], a).
+ *                    Then parent[r] = r.
+ *   4. oracle_mcomp: count tuples whose source is reached.
+ *   5. oracle_validate: the Graph500 tree-validation invariants V1..V6.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  uint64_t n;          /* number of vertices */
+  uint64_t m;          /* number of tuples */
+  const uint64_t* src; /* borrowed tuple arrays */
+  const uint64_t* dst;
+  uint64_t* off;       /* n+1 adjacency offsets */
+  uint64_t* adj;       /* adjacency lists (undirected, self-loops skipped, duplicates kept) */
+} oracle_graph;
+
+/* Step 1: counting sort of the tuple endpoints into an undirected adjacency. Returns NULL on
+ * allocation failure or an endpoint >= n. */
+oracle_graph* oracle_build(uint64_t n, uint64_t m, const uint64_t* src, const uint64_t* dst) {
+  oracle_graph* g = (oracle_graph*)calloc(1, sizeof(oracle_graph));
+  if (!g) return NULL;
+  g->n = n;
+  g->m = m;
+  g->src = src;
+  g->dst = dst;
+  g->off = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
+  if (!g->off) { free(g); return NULL; }
+  for (uint64_t k = 0; k < m; ++k) {
+    uint64_t a = src[k], b = dst[k];
+    if (a >= n || b >= n) { free(g->off); free(g); return NULL; }
+    if (a == b) continue;
+    g->off[a + 1] += 1; /* edge a -> b */
+    g->off[b + 1] += 1; /* its opposite b -> a */
+  }
+  for (uint64_t v = 0; v < n; ++v) g->off[v + 1] += g->off[v];
+  g->adj = (uint64_t*)malloc((g->off[n] ? g->off[n] : 1) * sizeof(uint64_t));
+  uint64_t* fill = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+  if (!g->adj || !fill) { free(g->adj); free(fill); free(g->off); free(g); return NULL; }
+  for (uint64_t v = 0; v < n; ++v) fill[v] = g->off[v];
+  for (uint64_t k = 0; k < m; ++k) {
+    uint64_t a = src[k], b = dst[k];
+    if (a == b) continue;
+    g->adj[fill[a]++] = b;
+    g->adj[fill[b]++] = a;
+  }
+  free(fill);
+  return g;
+}
+
+void oracle_free(oracle_graph* g) {
+  if (!g) return;
+  free(g->off);
+  free(g->adj);
+  free(g);
+}
+
+uint64_t oracle_num_adjacency(const oracle_graph* g) { return g->off[g->n]; }
+
+/* Number of distinct neighbours of v other than v (degree in G). Used to choose roots. */
+uint64_t oracle_degree(const oracle_graph* g, uint64_t v) {
+  return g->off[v + 1] - g->off[v];
+}
+
+/* Steps 2-3.  level[n], parent[n] are caller-allocated. Returns 0, or -2 if root >= n. */
+int oracle_bfs(const oracle_graph* g, uint64_t root, int32_t* level, int64_t* parent) {
+  const uint64_t n = g->n;
+  if (root >= n) return -2;
+  for (uint64_t v = 0; v < n; ++v) { level[v] = -1; parent[v] = -1; }
+  /* 2. FIFO BFS */
+  uint64_t* queue = (uint64_t*)malloc(n * sizeof(uint64_t));
+  if (!queue) return -3;
+  uint64_t head = 0, tail = 0;
+  level[root] = 0;
+  queue[tail++] = root;
+  while (head < tail) {
+    uint64_t u = queue[head++];
+    for (uint64_t e = g->off[u]; e < g->off[u + 1]; ++e) {
+      uint64_t v = g->adj[e];
+      if (level[v] < 0) {
+        level[v] = level[u] + 1;
+        queue[tail++] = v;
+      }
+    }
+  }
+  free(queue);
+  /* 3. parent = minimum neighbour one level up, from the tuple list in both orientations */
+  for (uint64_t k = 0; k < g->m; ++k) {
+    uint64_t a = g->src[k], b = g->dst[k];
+    if (a == b) continue;
+    if (level[a] >= 0 && level[b] == level[a] + 1) {
+      if (parent[b] < 0 || (uint64_t)parent[b] > a) parent[b] = (int64_t)a;
+    }
+    if (level[b] >= 0 && level[a] == level[b] + 1) {
+      if (parent[a] < 0 || (uint64_t)parent[a] > b) parent[a] = (int64_t)b;
+    }
+  }
+  parent[root] = (int64_t)root;
+  return 0;
+}
+
+/* Step 4: input tuples of the traversed component. */
+uint64_t oracle_mcomp(const oracle_graph* g, const int32_t* level) {
+  uint64_t c = 0;
+  for (uint64_t k = 0; k < g->m; ++k)
+    if (level[g->src[k]] >= 0) ++c;
+  return c;
+}
+
+/* Step 5: Graph500-style validation of (level, parent) for root r against the tuple list.
+ * Returns a bitmask of FAILED checks (0 = valid):
+ *   bit0 V1 level[r] == 0 and parent[r] == r
+ *   bit1 V2 every tree edge {parent[v], v}, v != r reached, is an input tuple (either orientation,
+ *           non-self-loop)
+ *   bit2 V3 level[v] == level[parent[v]] + 1 for reached v != r
+ *   bit3 V4 every non-self-loop tuple with one endpoint reached has both reached, |dlevel| <= 1
+ *   bit4 V5 reached set == component of r (union-find over the tuples); unreached v have
+ *           level == parent == -1; reached v have parent in [0, n)
+ *   bit5 V6 min rule: for every tuple (a,b), both orientations, level[a] == level[b]-1 implies
+ *           parent[b] <= a
+ * Streaming over the tuple list; does not need oracle_build (takes the arrays directly). */
+static uint64_t uf_find(uint64_t* p, uint64_t x) {
+  while (p[x] != x) { p[x] = p[p[x]]; x = p[x]; }
+  return x;
+}
+
+int oracle_validate(uint64_t n, uint64_t m, const uint64_t* src, const uint64_t* dst, uint64_t root,
+                    const int32_t* level, const int64_t* parent) {
+  int fail = 0;
+  if (root >= n) return 1;
+  /* V1 */
+  if (level[root] != 0 || parent[root] != (int64_t)root) fail |= 1;
+  /* V5 (part): consistent unreached / range of parents */
+  for (uint64_t v = 0; v < n; ++v) {
+    if (level[v] < 0) {
+      if (level[v] != -1 || parent[v] != -1) fail |= 16;
+    } else {
+      if (parent[v] < 0 || (uint64_t)parent[v] >= n) fail |= 16;
+    }
+  }
+  if (fail & 16) return fail; /* parent[] not usable as an index */
+  /* V3 */
+  for (uint64_t v = 0; v < n; ++v) {
+    if (v == root || level[v] < 0) continue;
+    uint64_t p = (uint64_t)parent[v];
+    if (level[p] < 0 || level[v] != level[p] + 1) fail |= 4;
+  }
+  /* V2: mark tree edges found among the tuples */
+  unsigned char* found = (unsigned char*)calloc(n ? n : 1, 1);
+  /* V5: union-find of the tuple graph */
+  uint64_t* uf = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+  if (!found || !uf) { free(found); free(uf); return 64; }
+  for (uint64_t v = 0; v < n; ++v) uf[v] = v;
+  for (uint64_t k = 0; k < m; ++k) {
+    uint64_t a = src[k], b = dst[k];
+    if (a >= n || b >= n) { fail |= 64; continue; }
+    if (a == b) continue;
+    /* V2 */
+    if (level[b] > 0 && (uint64_t)parent[b] == a) found[b] = 1;
+    if (level[a] > 0 && (uint64_t)parent[a] == b) found[a] = 1;
+    /* V4 */
+    if ((level[a] >= 0) != (level[b] >= 0)) fail |= 8;
+    else if (level[a] >= 0) {
+      int dl = level[a] - level[b];
+      if (dl > 1 || dl < -1) fail |= 8;
+    }
+    /* V6 */
+    if (level[a] >= 0 && level[b] == level[a] + 1 && (uint64_t)parent[b] > a) fail |= 32;
+    if (level[b] >= 0 && level[a] == level[b] + 1 && (uint64_t)parent[a] > b) fail |= 32;
+    /* V5 union */
+    uint64_t ra = uf_find(uf, a), rb = uf_find(uf, b);
+    if (ra != rb) uf[ra] = rb;
+  }
+  for (uint64_t v = 0; v < n; ++v)
+    if (v != root && level[v] > 0 && !found[v]) fail |= 2;
+  uint64_t rr = uf_find(uf, root);
+  for (uint64_t v = 0; v < n; ++v) {
+    int in_comp = (uf_find(uf, v) == rr);
+    if (in_comp != (level[v] >= 0)) fail |= 16;
+  }
+  free(found);
+  free(uf);
+  return fail;
+}
