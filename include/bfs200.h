@@ -1,0 +1,165 @@
+/*
+ * bfs200.h -- C ABI of libbfs200.so: level-synchronous top-down BFS over a 2D (R x C)
+ * partitioned adjacency matrix, B200 (sm_100a) native.  arXiv 1408.1605 ("the paper").
+ *
+ * Problem (Alg.2): given an undirected graph as a list of
+ * input tuples ("We turn the graph undirected by adding, for each edge, its
+ * opposite") and a root r, compute for every vertex v its BFS level (hop distance from r,
+ * -1 if unreachable) and its BFS-tree parent,
+ * the parent being fixed as the MINIMUM-id neighbour one level up (the deterministic parent
+ * claim of BASELINE.json's north_star; reading R1).
+ *
+ * Partition: R*C ranks form an R x C grid; rank r = j*R + i is P_ij; it owns the
+ * vertex block [r*block, (r+1)*block), block = Npad/(R*C), and stores the edge blocks
+ * (m*R+i, j), m = 0..C-1, as one CSC matrix of (Npad/R) x (Npad/C).
+ *
+ * Conventions for every call:
+ *   - Return value: BFS_OK (0) or a negative bfs_status.  bfs_last_error() gives a
+ *     thread-local detail string for the last failure on the calling thread.
+ *   - Pointers documented as "host or device" are classified with cudaPointerGetAttributes;
+ *     device pointers must be on the graph's device.
+ *   - All calls taking a bfs_graph* are COLLECTIVE over the R*C ranks when the graph was
+ *     created with the NCCL transport (every rank calls them in the same order with the same
+ *     scalar arguments).  With the loopback transport one process holds all R*C logical ranks
+ *     on one GPU and the calls are ordinary.
+ *   - A CUDA or NCCL failure is fatal for the graph: it returns BFS_ECUDA / BFS_ENCCL and
+ *     every later call on that graph returns BFS_ESTATE.
+ *   - No global mutable state besides the thread-local error string; distinct graphs may be
+ *     used from distinct threads.
+ */
+#ifndef BFS200_H
+#define BFS200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BFS_OK = 0,
+  BFS_EINVAL = -1, /* bad argument: null pointer, R*C mismatch, nverts too large, ...        */
+  BFS_ERANGE = -2, /* a vertex id (root, edge endpoint, query) is >= nverts                  */
+  BFS_ENOMEM = -3, /* device or host allocation failed                                       */
+  BFS_ECUDA = -4,  /* CUDA runtime error (graph becomes unusable)                            */
+  BFS_ENCCL = -5,  /* NCCL error (graph becomes unusable)                                    */
+  BFS_ESTATE = -6  /* graph unusable after an earlier fatal error, or call out of order      */
+} bfs_status;
+
+typedef struct bfs_graph bfs_graph; /* opaque; owned by the library until bfs_destroy */
+
+/* Transport.  loopback != 0: this process emulates all R*C ranks on `device` (collectives
+ * become device-to-device copies; for tests of the 2D logic on one GPU).  loopback == 0:
+ * one rank per process; `rank`/`nranks` are this process's place in the R*C grid and
+ * nccl_id is the ncclUniqueId made by rank 0 (bfs_nccl_unique_id) and broadcast by the
+ * caller (e.g. with torch.distributed).  R = C = 1 with loopback = 0 needs no NCCL. */
+typedef struct {
+  int rank;
+  int nranks;
+  int device;
+  int loopback;
+  unsigned char nccl_id[128];
+} bfs_comm;
+
+/* Tuning / execution options; zero-initialised means defaults. */
+typedef struct {
+  int edges_per_thread; /* E, consecutive edges per expansion thread; 0 -> 4;
+                           allowed 1, 2, 4, 8, 16 */
+  int phase_timing;     /* != 0: record CUDA events around every phase of every level; read
+                           them afterwards with bfs_level_times (does not synchronise) */
+  void* stream;         /* cudaStream_t all work is issued on; NULL -> a library-owned stream */
+} bfs_opts;
+
+/* Shape of this process's part of the partition. */
+typedef struct {
+  uint64_t nverts;       /* as passed to bfs_graph_create */
+  uint64_t npad;         /* nverts rounded up to a multiple of 32*R*C (padding = isolated)  */
+  uint64_t block;        /* npad / (R*C): vertices owned per rank                           */
+  int R, C;
+  int rank;              /* first rank held by this process (0 with loopback)               */
+  int nlocal;            /* ranks held by this process (R*C with loopback, else 1)          */
+  uint64_t first_vertex; /* rank * block: global id of output element 0                     */
+  uint64_t nout;         /* nlocal * block: length of the parent/level outputs of bfs_run   */
+  uint64_t nnz_local;    /* CSC entries held by this process (after dedup, no self-loops)   */
+  uint64_t ntuples;      /* input tuples seen by this process's create call                 */
+  uint64_t device_bytes; /* device memory held by the graph                                 */
+} bfs_info;
+
+/* Per-run counters (cheap; filled by bfs_run when stats != NULL). Sums over local ranks. */
+typedef struct {
+  int nlevels;               /* BFS levels executed (including the final empty one)        */
+  uint64_t edges_scanned;    /* CSC entries expanded (sum over levels of cumul[n])         */
+  uint64_t frontier_columns; /* frontier columns with local degree > 0, summed over levels  */
+  uint64_t reached;          /* owned vertices reached (level >= 0)                        */
+  uint64_t bytes_exchanged;  /* bytes sent by this process's ranks over the transport      */
+  uint64_t kernel_launches;  /* libbfs200 kernels launched by the call (CUB/NCCL excluded)  */
+} bfs_stats;
+
+/* Per-level phase times (milliseconds, CUDA events) of the last run with phase_timing. */
+typedef struct {
+  double expand_comm; /* column all-gather of the frontier bitmap        */
+  double scan;        /* frontier unpack + degree exclusive scan    */
+  double expand;      /* frontier expansion kernel                         (Alg.3)        */
+  double fold_comm;   /* row exchange of discovered-vertex bitmaps        */
+  double update;      /* frontier update + pack    */
+  double allreduce;   /* termination reduction + host read        */
+  uint64_t frontier;  /* frontier columns with degree > 0 (all local ranks) */
+  uint64_t edges;     /* CSC entries expanded (all local ranks)            */
+} bfs_level_record;
+
+/* ncclGetUniqueId into out[128] (call on rank 0 only). */
+int bfs_nccl_unique_id(unsigned char* out128);
+
+/* Build the partitioned graph.
+ *   src, dst  : host or device arrays of nedges global vertex ids (the tuples this process
+ *               contributes; with NCCL any split of the global list over ranks is allowed).
+ *               Borrowed for the duration of the call only.  Tuples are undirected: both
+ *               orientations are inserted; self-loops and duplicates are dropped
+ *               from the CSC but counted for m_comp.
+ *   nverts    : number of vertices, 1 <= nverts and npad < 2^32 (ids are stored as u32;
+ *               UINT32_MAX is the "no parent candidate" sentinel). Same on every rank.
+ *   R, C      : grid; R*C must equal comm->nranks (NCCL) -- with loopback any R, C >= 1.
+ *   comm      : transport (see bfs_comm); NULL means single GPU, device 0, R = C = 1.
+ *   opts      : NULL for defaults; copied.
+ *   out       : receives the graph.
+ * Errors: BFS_EINVAL (bad shape/args), BFS_ERANGE (endpoint >= nverts), BFS_ENOMEM,
+ *         BFS_ECUDA, BFS_ENCCL.  On error *out is NULL. */
+int bfs_graph_create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uint64_t nverts, int R, int C,
+                     const bfs_comm* comm, const bfs_opts* opts, bfs_graph** out);
+
+int bfs_graph_info(const bfs_graph* g, bfs_info* info);
+
+/* Replace the options (E, phase timing, stream) used by later runs. */
+int bfs_set_opts(bfs_graph* g, const bfs_opts* opts);
+
+/* Degree of global vertex v in the simple undirected graph (distinct neighbours other than v).
+ * Used by the harness to sample roots with degree >= 1. BFS_ERANGE if v >= nverts. */
+int bfs_degree(bfs_graph* g, uint64_t v, uint64_t* degree);
+
+/* One BFS from `root` (Alg.2).  Writes info.nout entries of parent[] (int64 global ids) and
+ * level[] (int32), element t describing global vertex info.first_vertex + t; either may be a
+ * host or a device pointer (or NULL to skip).  Unreached vertices (and padding vertices) get
+ * level = -1, parent = -1; parent[root] = root.  Outputs are written only on success.
+ * BFS_ERANGE if root >= nverts (outputs untouched).  Every rank passes the same root.
+ * Returns after the outputs are complete (the stream is synchronised). */
+int bfs_run(bfs_graph* g, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats);
+
+/* m_comp of the last run: number of input tuples whose source was reached, duplicates and
+ * self-loops included (the TEPS numerator).  Summed over all ranks. */
+int bfs_mcomp(bfs_graph* g, uint64_t* m_comp);
+
+/* Per-level phase times of the last run (requires opts.phase_timing). Writes up to
+ * max_levels records and the level count to *nlevels. Synchronises on the recorded events. */
+int bfs_level_times(bfs_graph* g, bfs_level_record* out, int max_levels, int* nlevels);
+
+/* NULL-safe, idempotent for NULL.  Collective with NCCL. */
+void bfs_destroy(bfs_graph* g);
+
+const char* bfs_strerror(int status);
+const char* bfs_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BFS200_H */

@@ -1,0 +1,210 @@
+"""Thin ctypes binding of libbfs200.so (include/bfs200.h).  Argument marshalling only.
+
+Every step of the BFS runs in the CUDA library; there is no CPU fallback.  If the library is
+missing or no GPU is present, the calls raise.
+
+Buffers may be numpy arrays (host) or torch tensors (host or CUDA); the library classifies
+pointers itself (cudaPointerGetAttributes).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+_LIB = _build.LIB
+
+BFS_OK, BFS_EINVAL, BFS_ERANGE, BFS_ENOMEM, BFS_ECUDA, BFS_ENCCL, BFS_ESTATE = 0, -1, -2, -3, -4, -5, -6
+
+
+class BfsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+class Comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("device", ctypes.c_int),
+                ("loopback", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("edges_per_thread", ctypes.c_int), ("phase_timing", ctypes.c_int), ("stream", ctypes.c_void_p)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("nverts", ctypes.c_uint64), ("npad", ctypes.c_uint64), ("block", ctypes.c_uint64),
+                ("R", ctypes.c_int), ("C", ctypes.c_int), ("rank", ctypes.c_int), ("nlocal", ctypes.c_int),
+                ("first_vertex", ctypes.c_uint64), ("nout", ctypes.c_uint64), ("nnz_local", ctypes.c_uint64),
+                ("ntuples", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("nlevels", ctypes.c_int), ("edges_scanned", ctypes.c_uint64),
+                ("frontier_columns", ctypes.c_uint64), ("reached", ctypes.c_uint64),
+                ("bytes_exchanged", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64)]
+
+
+class LevelRecord(ctypes.Structure):
+    _fields_ = [("expand_comm", ctypes.c_double), ("scan", ctypes.c_double), ("expand", ctypes.c_double),
+                ("fold_comm", ctypes.c_double), ("update", ctypes.c_double), ("allreduce", ctypes.c_double),
+                ("frontier", ctypes.c_uint64), ("edges", ctypes.c_uint64)]
+
+
+EXPORTS = ["bfs_nccl_unique_id", "bfs_graph_create", "bfs_graph_info", "bfs_set_opts", "bfs_degree", "bfs_run",
+           "bfs_mcomp", "bfs_level_times", "bfs_destroy", "bfs_strerror", "bfs_last_error"]
+
+_lib = None
+
+
+def lib(build: bool = False):
+    """Load libbfs200.so (building it first if `build`); raises if it cannot be loaded."""
+    global _lib
+    if _lib is None:
+        if build:
+            _build.build_bfs()
+        if not os.path.exists(_LIB):
+            raise RuntimeError(f"{_LIB} not built: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(_LIB)
+        p, u64, i = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
+        L.bfs_nccl_unique_id.argtypes = [p]
+        L.bfs_graph_create.argtypes = [p, p, u64, u64, i, i, ctypes.POINTER(Comm), ctypes.POINTER(Opts),
+                                       ctypes.POINTER(p)]
+        L.bfs_graph_info.argtypes = [p, ctypes.POINTER(Info)]
+        L.bfs_set_opts.argtypes = [p, ctypes.POINTER(Opts)]
+        L.bfs_degree.argtypes = [p, u64, ctypes.POINTER(u64)]
+        L.bfs_run.argtypes = [p, u64, p, p, ctypes.POINTER(Stats)]
+        L.bfs_mcomp.argtypes = [p, ctypes.POINTER(u64)]
+        L.bfs_level_times.argtypes = [p, ctypes.POINTER(LevelRecord), i, ctypes.POINTER(i)]
+        L.bfs_destroy.argtypes = [p]
+        L.bfs_destroy.restype = None
+        L.bfs_strerror.argtypes = [i]
+        L.bfs_strerror.restype = ctypes.c_char_p
+        L.bfs_last_error.argtypes = []
+        L.bfs_last_error.restype = ctypes.c_char_p
+        for name in EXPORTS[:-3]:
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != BFS_OK:
+        L = lib()
+        raise BfsError(rc, f"{L.bfs_strerror(rc).decode()}: {L.bfs_last_error().decode()}")
+
+
+def _ptr(x):
+    """Raw address of a numpy array / torch tensor (contiguous) or None."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().bfs_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def make_comm(rank=0, nranks=1, device=0, loopback=True, nccl_id: bytes | None = None) -> Comm:
+    c = Comm()
+    c.rank, c.nranks, c.device, c.loopback = rank, nranks, device, 1 if loopback else 0
+    if nccl_id is not None:
+        ctypes.memmove(c.nccl_id, nccl_id, 128)
+    return c
+
+
+def make_opts(edges_per_thread=4, phase_timing=False, stream=None) -> Opts:
+    o = Opts()
+    o.edges_per_thread = int(edges_per_thread)
+    o.phase_timing = 1 if phase_timing else 0
+    if stream is not None:
+        o.stream = stream if isinstance(stream, int) else getattr(stream, "cuda_stream", None)
+    return o
+
+
+class Graph:
+    """A partitioned graph resident on the GPU (bfs_graph_create .. bfs_destroy)."""
+
+    def __init__(self, src, dst, nverts, R=1, C=1, comm: Comm | None = None, opts: Opts | None = None):
+        L = lib()
+        n = int(len(src))
+        if int(len(dst)) != n:
+            raise ValueError("src/dst length mismatch")
+        for a in (src, dst):
+            dt = getattr(a, "dtype", None)
+            if str(dt) not in ("uint64", "torch.uint64", "int64", "torch.int64"):
+                raise TypeError(f"edge arrays must be 64-bit integers, got {dt}")
+        h = ctypes.c_void_p()
+        _check(L.bfs_graph_create(_ptr(src), _ptr(dst), n, int(nverts), int(R), int(C),
+                                  ctypes.byref(comm) if comm is not None else None,
+                                  ctypes.byref(opts) if opts is not None else None, ctypes.byref(h)))
+        self._h = h
+        self.info = self.get_info()
+
+    def get_info(self) -> Info:
+        inf = Info()
+        _check(lib().bfs_graph_info(self._h, ctypes.byref(inf)))
+        return inf
+
+    def set_opts(self, opts: Opts):
+        _check(lib().bfs_set_opts(self._h, ctypes.byref(opts)))
+
+    def degree(self, v: int) -> int:
+        out = ctypes.c_uint64()
+        _check(lib().bfs_degree(self._h, int(v), ctypes.byref(out)))
+        return int(out.value)
+
+    def run(self, root: int, parent=None, level=None, want_stats=True):
+        """BFS from root into the given buffers (numpy/torch, host or device). Returns Stats."""
+        st = Stats()
+        _check(lib().bfs_run(self._h, int(root), _ptr(parent), _ptr(level),
+                             ctypes.byref(st) if want_stats else None))
+        return st
+
+    def bfs(self, root: int):
+        """Convenience: (level int32[nout], parent int64[nout]) as host numpy arrays."""
+        parent = np.empty(self.info.nout, dtype=np.int64)
+        level = np.empty(self.info.nout, dtype=np.int32)
+        self.run(root, parent, level)
+        return level, parent
+
+    def mcomp(self) -> int:
+        out = ctypes.c_uint64()
+        _check(lib().bfs_mcomp(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    def level_times(self, max_levels=256):
+        recs = (LevelRecord * max_levels)()
+        n = ctypes.c_int()
+        _check(lib().bfs_level_times(self._h, recs, max_levels, ctypes.byref(n)))
+        return [recs[i] for i in range(min(n.value, max_levels))]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bfs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,103 @@
+// bfs_internal.h -- internal data structures of libbfs200 (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bfs200.h"
+
+namespace bfs200 {
+
+constexpr uint32_t kNoPred = 0xFFFFFFFFu;  // "no candidate" sentinel in pred[] (R11)
+constexpr int kScanTileWords = 2048;       // bitmap words per unpack/scan tile (65536 vertices)
+constexpr int kScanThreads = 256;          // 8 words per thread
+constexpr int kExpandThreads = 256;
+constexpr int kMaxLevels = 4096;
+
+// Device-side per-level counters written by the scan kernels (read by the expansion kernel,
+// so the host never needs the frontier size to launch it).
+struct LevelInfo {
+  unsigned long long n;      // frontier columns with local degree > 0
+  unsigned long long edges;  // cumul[n]
+  unsigned long long newv;   // vertices discovered by the update (this rank)
+  unsigned long long pad;
+};
+
+// Geometry of the 2D partition (index maps SPEC.md S:109-148).
+struct Geom {
+  uint64_t nverts, npad, block;
+  int R, C;
+  uint64_t ncols() const { return (uint64_t)R * block; }  // N/C local columns
+  uint64_t nrows() const { return (uint64_t)C * block; }  // N/R local rows
+  uint64_t words_block() const { return block / 32; }
+};
+
+// One P_ij.  All pointers are device pointers on the graph's device.
+struct Rank {
+  int r, i, j;        // r = j*R + i
+  uint64_t nnz = 0;   // CSC entries
+  unsigned long long* col = nullptr;  // [ncols+1] column offsets (u64: nnz can exceed 2^32)
+  uint32_t* row = nullptr;    // [nnz] local row ids, ascending within each column
+  uint32_t* tdeg = nullptr;   // [block] input tuples whose source is the owned vertex (m_comp)
+  // per-search state
+  uint32_t* visited = nullptr;   // [nrows/32] visited bitmap over ALL local rows
+  uint32_t* disc = nullptr;      // [nrows/32] rows discovered in this level, C segments of block bits
+  uint32_t* recv = nullptr;      // [C * block/32] fold receive buffer (segment c from P_ic); C>1 only
+  uint32_t* all_front = nullptr; // [ncols/32] gathered frontier bitmap; own segment i = own frontier
+  uint32_t* pred = nullptr;      // [nrows] min parent candidate (global id) per local row
+  int32_t* level = nullptr;      // [block] owned levels
+  uint8_t* winner = nullptr;     // [block] grid column that supplied the parent (C>1 only)
+  uint32_t* flist = nullptr;     // [ncols] frontier columns with degree>0, ascending
+  unsigned long long* rowoff = nullptr;  // [ncols] col[flist[k]]
+  unsigned long long* cumul = nullptr;   // [ncols+1] exclusive scan of degrees
+  uint32_t* tile_k = nullptr;            // [nnz/256 + 2] first frontier index of every expansion tile
+  uint32_t* tile_cnt = nullptr;          // [ntiles] per-tile frontier count
+  unsigned long long* tile_sum = nullptr;// [ntiles] per-tile degree sum
+  uint32_t* tile_cnt_off = nullptr;
+  unsigned long long* tile_sum_off = nullptr;
+  LevelInfo* info = nullptr;             // [1]
+  int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution
+  // parent resolution (C>1)
+  uint32_t* req = nullptr;       // [C * block/32] request bitmaps: rows whose parent lives at P_ic
+  uint32_t* reqin = nullptr;     // [C * block/32] requests received from P_ic (rows of segment c)
+  uint32_t* off_in = nullptr;    // [C*block/32 + 1] exclusive popcount scan of reqin
+  uint32_t* off_req = nullptr;   // [C*block/32 + 1] exclusive popcount scan of req
+  void* scan_tmp = nullptr;      // CUB temp for the popcount scans
+  size_t scan_tmp_bytes = 0;
+  uint32_t* resp = nullptr;      // [nrows] compacted responses (sent)
+  uint32_t* respin = nullptr;    // [nrows] compacted responses (received)
+  unsigned long long* scratch = nullptr;  // small reduction scratch
+};
+
+struct Graph {
+  Geom g{};
+  int device = 0;
+  int loopback = 1;
+  int world_rank = 0, world_size = 1;
+  bool owns_stream = false;
+  cudaStream_t stream = nullptr;
+  bfs_opts opts{};
+  bool broken = false;
+  std::vector<Rank> ranks;  // local ranks (all R*C with loopback)
+  std::vector<void*> allocs;  // graph-lifetime device allocations
+  LevelInfo* infos = nullptr; // [nlocal] device, one per local rank
+  LevelInfo* h_infos = nullptr; // pinned mirror
+  unsigned long long* dscratch = nullptr; // [16] device scratch for reductions
+  // NCCL (loopback == 0 and R*C > 1)
+  ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+  unsigned long long* h_scratch = nullptr;  // pinned [16]
+  uint64_t ntuples = 0;
+  uint64_t device_bytes = 0;
+  int last_levels = 0;
+  bool has_run = false;
+  // phase-timing events: [level][phase boundary]
+  std::vector<cudaEvent_t> ev;
+  int ev_levels = 0;
+  std::vector<uint64_t> lvl_frontier, lvl_edges;
+};
+
+}  // namespace bfs200

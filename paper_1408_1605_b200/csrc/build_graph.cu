@@ -1,0 +1,289 @@
+// build_graph.cu -- graph construction: tuples -> 2D partition -> per-rank CSC (not timed).
+//
+// PAPER.md P:300-303 ("the graph is partitioned as described in Section 2DPart")
+// (symmetrise), P:275-291 (local (N/R) x (N/C) matrix stored as CSC: `col` offsets + `row`
+// indices).  Each tuple (a, b), a != b, is inserted as edge a->b and b->a; edge u->v goes to
+// P_ij with i = (v/block) mod R, j = u/(N/C) as column
+// local_col(u) = u mod N/C and row local_row(v) = (v/block/R)*block + v mod block.
+// Duplicates collapse and self-loops are dropped; rows are ascending within a
+// column.  tdeg[v] counts every input tuple with source v (the m_comp numerator,
+// P:695-698), duplicates and self-loops included.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "engine.h"
+
+namespace bfs200 {
+
+typedef unsigned long long ull;
+
+struct PartMap {
+  uint64_t block, ncols, nverts;
+  int R, C, rbits;
+  __device__ __forceinline__ int dest(uint64_t u, uint64_t v) const {
+    const int i = (int)((v / block) % (uint64_t)R);
+    const int j = (int)(u / ncols);
+    return j * R + i;
+  }
+  __device__ __forceinline__ ull key(uint64_t u, uint64_t v) const {
+    const uint64_t lc = u % ncols;
+    const uint64_t lr = (v / block / (uint64_t)R) * block + v % block;
+    return ((ull)lc << rbits) | (ull)lr;
+  }
+};
+
+constexpr int kBuildThreads = 256;
+constexpr int kBuildPer = 8;  // tuples per thread per CTA chunk
+constexpr int kMaxP = 64;
+
+// count directed entries per destination rank; validate ids; tuple-source histogram
+__global__ void __launch_bounds__(kBuildThreads) k_count(const uint64_t* src, const uint64_t* dst, uint64_t m,
+                                                         PartMap pm, int P, ull* counts, uint32_t* tdeg_all,
+                                                         int* err) {
+  __shared__ unsigned int sc[kMaxP];
+  for (int q = threadIdx.x; q < P; q += blockDim.x) sc[q] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kBuildThreads * kBuildPer;
+  for (int q = 0; q < kBuildPer; ++q) {
+    const uint64_t k = base + (uint64_t)q * kBuildThreads + threadIdx.x;
+    if (k >= m) break;
+    const uint64_t a = src[k], b = dst[k];
+    if (a >= pm.nverts || b >= pm.nverts) {
+      atomicOr(err, 1);
+      continue;
+    }
+    if (tdeg_all) atomicAdd(tdeg_all + a, 1u);
+    if (a == b) continue;
+    atomicAdd(&sc[pm.dest(a, b)], 1u);
+    atomicAdd(&sc[pm.dest(b, a)], 1u);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < P; q += blockDim.x)
+    if (sc[q]) atomicAdd(counts + q, (ull)sc[q]);
+}
+
+// scatter keys into per-destination buckets; cursors[r] starts at the bucket offset
+__global__ void __launch_bounds__(kBuildThreads) k_scatter(const uint64_t* src, const uint64_t* dst, uint64_t m,
+                                                           PartMap pm, int P, ull* cursors, ull* keys) {
+  __shared__ unsigned int sc[kMaxP];
+  __shared__ ull sbase[kMaxP];
+  for (int q = threadIdx.x; q < P; q += blockDim.x) sc[q] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kBuildThreads * kBuildPer;
+  uint64_t a[kBuildPer], b[kBuildPer];
+  unsigned int pos1[kBuildPer], pos2[kBuildPer];
+  int d1[kBuildPer], d2[kBuildPer];
+  for (int q = 0; q < kBuildPer; ++q) {
+    const uint64_t k = base + (uint64_t)q * kBuildThreads + threadIdx.x;
+    d1[q] = -1;
+    if (k >= m) continue;
+    a[q] = src[k];
+    b[q] = dst[k];
+    if (a[q] == b[q]) continue;
+    d1[q] = pm.dest(a[q], b[q]);
+    d2[q] = pm.dest(b[q], a[q]);
+    pos1[q] = atomicAdd(&sc[d1[q]], 1u);
+    pos2[q] = atomicAdd(&sc[d2[q]], 1u);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < P; q += blockDim.x) sbase[q] = sc[q] ? atomicAdd(cursors + q, (ull)sc[q]) : 0ull;
+  __syncthreads();
+  for (int q = 0; q < kBuildPer; ++q) {
+    if (d1[q] < 0) continue;
+    keys[sbase[d1[q]] + pos1[q]] = pm.key(a[q], b[q]);
+    keys[sbase[d2[q]] + pos2[q]] = pm.key(b[q], a[q]);
+  }
+}
+
+__global__ void k_keys_to_rows(const ull* keys, uint64_t n, ull rmask, uint32_t* row) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    row[t] = (uint32_t)(keys[t] & rmask);
+}
+
+// col[c] = first position with key >= c << rbits (lower bound), c in [0, ncols]
+__global__ void k_col_offsets(const ull* keys, uint64_t n, int rbits, uint64_t ncols, ull* col) {
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= ncols;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const ull target = (ull)c << rbits;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    col[c] = lo;
+  }
+}
+
+static int bits_for(uint64_t n) {  // bits to represent values < n
+  int b = 0;
+  while (b < 64 && (1ull << b) < n) ++b;
+  return b;
+}
+
+// Sorted/deduplicated CSC for one rank from its bucket of keys (consumed: used as scratch).
+static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits) {
+  cudaStream_t s = G.stream;
+  const Geom& g = G.g;
+  const int kbits = rbits + bits_for(g.ncols());
+  Scratch sc;
+  ull* sorted = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, tmp2 = 0;
+  ull* nsel = nullptr;
+  int rc = BFS_OK;
+  if (n) {
+    CKR(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys, (uint64_t)n, 0, kbits, s));
+    CKR(cub::DeviceSelect::Unique(nullptr, tmp2, keys, keys, nsel, (uint64_t)n, s));
+    tmp_bytes = tmp_bytes > tmp2 ? tmp_bytes : tmp2;
+    CKR(sc.alloc(&sorted, n * sizeof(ull)));
+    CKR(sc.alloc(&tmp, tmp_bytes));
+    CKR(sc.alloc(&nsel, sizeof(ull)));
+    CKR(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (uint64_t)n, 0, kbits, s));
+    CKR(cub::DeviceSelect::Unique(tmp, tmp_bytes, sorted, keys, nsel, (uint64_t)n, s));
+    ull h_nsel = 0;
+    CKR(cudaMemcpyAsync(&h_nsel, nsel, sizeof(ull), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+    sc.release(sorted);
+    sc.release(tmp);
+    sc.release(nsel);
+    rk.nnz = h_nsel;
+  } else {
+    rk.nnz = 0;
+  }
+  rc = G_alloc(G, (void**)&rk.row, (rk.nnz ? rk.nnz : 1) * sizeof(uint32_t));
+  if (rc) return rc;
+  rc = G_alloc(G, (void**)&rk.col, (g.ncols() + 1) * sizeof(ull));
+  if (rc) return rc;
+  if (rk.nnz) {
+    k_keys_to_rows<<<4096, 256, 0, s>>>(keys, rk.nnz, (rbits >= 64) ? ~0ull : ((1ull << rbits) - 1), rk.row);
+    CKR(cudaGetLastError());
+  }
+  const uint64_t nc = g.ncols() + 1;
+  k_col_offsets<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(keys, rk.nnz, rbits, g.ncols(), rk.col);
+  CKR(cudaGetLastError());
+  CKR(cudaStreamSynchronize(s));
+  return BFS_OK;
+}
+
+// Build every local rank's CSC and tdeg.  src/dst: host or device arrays of m tuples.
+int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) {
+  cudaStream_t s = G.stream;
+  const Geom& g = G.g;
+  const int P = g.R * g.C;
+  if (P > kMaxP) return set_err(BFS_EINVAL, "R*C must be <= 64");
+  PartMap pm{g.block, g.ncols(), g.nverts, g.R, g.C, bits_for(g.nrows())};
+  const bool src_dev = is_device_ptr(src), dst_dev = is_device_ptr(dst);
+  if (src_dev != dst_dev) return set_err(BFS_EINVAL, "src and dst must both be host or both device pointers");
+
+  // ---- tuple-source histogram (whole vertex range) and per-destination counts
+  Scratch sc;
+  uint32_t* tdeg_all = nullptr;
+  ull* counts = nullptr;
+  int* err = nullptr;
+  CKR(sc.alloc(&tdeg_all, g.npad * sizeof(uint32_t)));
+  CKR(sc.alloc(&counts, 2 * kMaxP * sizeof(ull)));
+  CKR(sc.alloc(&err, sizeof(int)));
+  CKR(cudaMemsetAsync(tdeg_all, 0, g.npad * sizeof(uint32_t), s));
+  CKR(cudaMemsetAsync(counts, 0, 2 * kMaxP * sizeof(ull), s));
+  CKR(cudaMemsetAsync(err, 0, sizeof(int), s));
+  const uint64_t chunk = src_dev ? (m ? m : 1) : (1ull << 26);
+  uint64_t* stage_s = nullptr;
+  uint64_t* stage_d = nullptr;
+  if (!src_dev && m) {
+    CKR(sc.alloc(&stage_s, chunk * sizeof(uint64_t)));
+    CKR(sc.alloc(&stage_d, chunk * sizeof(uint64_t)));
+  }
+  auto for_chunks = [&](auto&& fn) -> int {
+    for (uint64_t k0 = 0; k0 < m; k0 += chunk) {
+      const uint64_t len = (m - k0 < chunk) ? (m - k0) : chunk;
+      const uint64_t* ps = src + k0;
+      const uint64_t* pd = dst + k0;
+      if (!src_dev) {
+        CKR(cudaMemcpyAsync(stage_s, ps, len * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        CKR(cudaMemcpyAsync(stage_d, pd, len * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        ps = stage_s;
+        pd = stage_d;
+      }
+      const uint64_t per = (uint64_t)kBuildThreads * kBuildPer;
+      fn(ps, pd, len, (unsigned)((len + per - 1) / per));
+      CKR(cudaGetLastError());
+      if (!src_dev) CKR(cudaStreamSynchronize(s));
+    }
+    return BFS_OK;
+  };
+  int rc = for_chunks([&](const uint64_t* ps, const uint64_t* pd, uint64_t len, unsigned grid) {
+    k_count<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, counts, tdeg_all, err);
+  });
+  if (rc) return rc;
+  ull h_counts[kMaxP];
+  int h_err = 0;
+  CKR(cudaMemcpyAsync(h_counts, counts, P * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  CKR(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CKR(cudaStreamSynchronize(s));
+  if (G.world_size > 1) {
+    int any_err = h_err;
+    rc = comm_allreduce_int_max(G, &any_err);
+    if (rc) return rc;
+    h_err = any_err;
+  }
+  if (h_err) return set_err(BFS_ERANGE, "an edge endpoint is >= nverts");
+
+  // ---- bucket keys by destination rank
+  ull offs[kMaxP + 1];
+  offs[0] = 0;
+  for (int q = 0; q < P; ++q) offs[q + 1] = offs[q] + h_counts[q];
+  ull* keys = nullptr;
+  CKR(sc.alloc(&keys, (offs[P] ? offs[P] : 1) * sizeof(ull)));
+  ull* cursors = counts + kMaxP;
+  CKR(cudaMemcpyAsync(cursors, offs, P * sizeof(ull), cudaMemcpyHostToDevice, s));
+  rc = for_chunks([&](const uint64_t* ps, const uint64_t* pd, uint64_t len, unsigned grid) {
+    k_scatter<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, cursors, keys);
+  });
+  if (rc) return rc;
+  CKR(cudaStreamSynchronize(s));
+  if (stage_s) { sc.release(stage_s); sc.release(stage_d); stage_s = stage_d = nullptr; }
+
+  if (G.world_size == 1) {
+    // loopback (or 1x1): every bucket is local
+    for (Rank& rk : G.ranks) {
+      rc = csc_from_keys(G, rk, keys + offs[rk.r], h_counts[rk.r], pm.rbits);
+      if (rc) return rc;
+      rc = G_alloc(G, (void**)&rk.tdeg, g.block * sizeof(uint32_t));
+      if (rc) return rc;
+      CKR(cudaMemcpyAsync(rk.tdeg, tdeg_all + (uint64_t)rk.r * g.block, g.block * sizeof(uint32_t),
+                          cudaMemcpyDeviceToDevice, s));
+    }
+    CKR(cudaStreamSynchronize(s));
+    sc.release(keys);
+  } else {
+    // NCCL: exchange bucket sizes, then the buckets (grouped send/recv over the world comm)
+    Rank& rk = G.ranks[0];
+    ull* recv_counts = nullptr;
+    CKR(sc.alloc(&recv_counts, kMaxP * sizeof(ull)));
+    rc = comm_exchange_counts(G, counts /*device counts[P]*/, recv_counts);
+    if (rc) return rc;
+    ull h_rc[kMaxP];
+    CKR(cudaMemcpyAsync(h_rc, recv_counts, P * sizeof(ull), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+    ull roffs[kMaxP + 1];
+    roffs[0] = 0;
+    for (int q = 0; q < P; ++q) roffs[q + 1] = roffs[q] + h_rc[q];
+    ull* rkeys = nullptr;
+    CKR(sc.alloc(&rkeys, (roffs[P] ? roffs[P] : 1) * sizeof(ull)));
+    rc = comm_alltoallv_u64(G, keys, offs, h_counts, rkeys, roffs, h_rc);
+    if (rc) return rc;
+    CKR(cudaStreamSynchronize(s));
+    sc.release(keys);
+    rc = csc_from_keys(G, rk, rkeys, roffs[P], pm.rbits);
+    sc.release(rkeys);
+    if (rc) return rc;
+    rc = G_alloc(G, (void**)&rk.tdeg, g.block * sizeof(uint32_t));
+    if (rc) return rc;
+    rc = comm_reduce_scatter_u32(G, tdeg_all, rk.tdeg, g.block);
+    if (rc) return rc;
+    CKR(cudaStreamSynchronize(s));
+  }
+  return BFS_OK;
+}
+
+}  // namespace bfs200

@@ -1,0 +1,675 @@
+// engine.cu -- libbfs200 C ABI: graph lifetime, the Alg.2 level loop, the expand / fold /
+// termination transport (loopback copies or NCCL over NVLink) and the deferred parent exchange.
+//
+// Level loop (Alg.2), per level lvl = 1, 2, ...:
+//   expand_comm   column all-gather of the owned frontier bitmaps
+//   scan          K3 unpack + degree exclusive scan
+//   expand        K1 frontier expansion                                       (Alg.3)
+//   fold_comm     row exchange of the discovered-row bitmap segments
+//   update        K2 OR / filter / level / next frontier
+//   allreduce     termination: total new vertices; stop when 0
+// After the loop the parents discovered by other grid columns are fetched once (P:47-49,
+// P:625-627): the owner requests, by bitmap, the rows whose lowest sending
+// column was c from P_ic, which answers with its pred[] entries in ascending row order.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "engine.h"
+#include "kernels.cuh"
+
+namespace bfs200 {
+
+typedef unsigned long long ull;
+
+static thread_local std::string tl_err;
+
+int set_err(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  tl_err = buf;
+  return status;
+}
+
+int cuda_fail(Graph& G, cudaError_t e, const char* what, const char* file, int line) {
+  G.broken = true;
+  return set_err(e == cudaErrorMemoryAllocation ? BFS_ENOMEM : BFS_ECUDA, "CUDA error %s (%s) at %s:%d: %s",
+                 cudaGetErrorName(e), cudaGetErrorString(e), file, line, what);
+}
+
+int nccl_fail(Graph& G, ncclResult_t r, const char* what, const char* file, int line) {
+  G.broken = true;
+  return set_err(BFS_ENCCL, "NCCL error %d (%s) at %s:%d: %s", (int)r, ncclGetErrorString(r), file, line, what);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int G_alloc(Graph& G, void** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return set_err(BFS_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  G.allocs.push_back(q);
+  G.device_bytes += bytes;
+  *p = q;
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ NCCL transport helpers
+int comm_allreduce_int_max(Graph& G, int* v) {
+  int* d = reinterpret_cast<int*>(G.dscratch);
+  CKR(cudaMemcpyAsync(d, v, sizeof(int), cudaMemcpyHostToDevice, G.stream));
+  NKR(ncclAllReduce(d, d, 1, ncclInt32, ncclMax, G.world, G.stream));
+  CKR(cudaMemcpyAsync(v, d, sizeof(int), cudaMemcpyDeviceToHost, G.stream));
+  CKR(cudaStreamSynchronize(G.stream));
+  return BFS_OK;
+}
+
+int comm_exchange_counts(Graph& G, const ull* send_counts, ull* recv_counts) {
+  const int P = G.world_size;
+  NKR(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    NKR(ncclSend(send_counts + q, 1, ncclUint64, q, G.world, G.stream));
+    NKR(ncclRecv(recv_counts + q, 1, ncclUint64, q, G.world, G.stream));
+  }
+  NKR(ncclGroupEnd());
+  return BFS_OK;
+}
+
+int comm_alltoallv_u64(Graph& G, const ull* send, const ull* soff, const ull* scnt, ull* recv, const ull* roff,
+                       const ull* rcnt) {
+  const int P = G.world_size, me = G.world_rank;
+  if (scnt[me]) CKR(cudaMemcpyAsync(recv + roff[me], send + soff[me], scnt[me] * sizeof(ull), cudaMemcpyDeviceToDevice,
+                                    G.stream));
+  NKR(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    if (scnt[q]) NKR(ncclSend(send + soff[q], scnt[q], ncclUint64, q, G.world, G.stream));
+    if (rcnt[q]) NKR(ncclRecv(recv + roff[q], rcnt[q], ncclUint64, q, G.world, G.stream));
+  }
+  NKR(ncclGroupEnd());
+  return BFS_OK;
+}
+
+int comm_reduce_scatter_u32(Graph& G, const uint32_t* full, uint32_t* mine, uint64_t block) {
+  NKR(ncclReduceScatter(full, mine, block, ncclUint32, ncclSum, G.world, G.stream));
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ per-level exchanges
+// expand: every rank of grid column j receives the owned-frontier segment of every other rank
+// of the column; segment i of all_front = frontier of P_ij (local column order).
+static int expand_exchange(Graph& G) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  if (g.R == 1) return BFS_OK;
+  if (G.world_size == 1) {
+    for (Rank& dst : G.ranks)
+      for (int i2 = 0; i2 < g.R; ++i2) {
+        if (i2 == dst.i) continue;
+        const Rank& src = G.ranks[dst.j * g.R + i2];
+        CKR(cudaMemcpyAsync(dst.all_front + i2 * W, src.all_front + i2 * W, W * 4, cudaMemcpyDeviceToDevice,
+                            G.stream));
+      }
+  } else {
+    Rank& rk = G.ranks[0];
+    NKR(ncclAllGather(rk.all_front + (uint64_t)rk.i * W, rk.all_front, W, ncclUint32, G.colc, G.stream));
+  }
+  return BFS_OK;
+}
+
+// fold: P_ij receives from every P_ic (c != j) the segment j of its discovered-row bitmap
+// (the rows it owns); the OR and the winner are taken by K2.
+static int fold_exchange(Graph& G) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  if (g.C == 1) return BFS_OK;
+  if (G.world_size == 1) {
+    for (Rank& dst : G.ranks)
+      for (int c = 0; c < g.C; ++c) {
+        if (c == dst.j) continue;
+        const Rank& src = G.ranks[c * g.R + dst.i];
+        CKR(cudaMemcpyAsync(dst.recv + c * W, src.disc + (uint64_t)dst.j * W, W * 4, cudaMemcpyDeviceToDevice,
+                            G.stream));
+      }
+  } else {
+    Rank& rk = G.ranks[0];
+    NKR(ncclGroupStart());
+    for (int c = 0; c < g.C; ++c) {
+      if (c == rk.j) continue;
+      NKR(ncclSend(rk.disc + (uint64_t)c * W, W, ncclUint32, c, G.rowc, G.stream));
+      NKR(ncclRecv(rk.recv + (uint64_t)c * W, W, ncclUint32, c, G.rowc, G.stream));
+    }
+    NKR(ncclGroupEnd());
+  }
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ graph lifetime
+static int alloc_state(Graph& G, Rank& rk) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
+  const uint64_t ntiles = (cw + kScanTileWords - 1) / kScanTileWords;
+  int rc;
+#define AL(ptr, bytes)                                  \
+  if ((rc = G_alloc(G, (void**)&(ptr), (bytes))) != 0) \
+    return rc;
+  AL(rk.visited, rw * 4);
+  AL(rk.disc, rw * 4);
+  AL(rk.all_front, cw * 4);
+  AL(rk.pred, g.nrows() * 4);
+  AL(rk.level, g.block * 4);
+  AL(rk.flist, g.ncols() * 4);
+  AL(rk.rowoff, g.ncols() * 8);
+  AL(rk.cumul, (g.ncols() + 1) * 8);
+  AL(rk.tile_k, (rk.nnz / 256 + 2) * 4);
+  AL(rk.tile_cnt, ntiles * 4);
+  AL(rk.tile_sum, ntiles * 8);
+  AL(rk.tile_cnt_off, ntiles * 4);
+  AL(rk.tile_sum_off, ntiles * 8);
+  AL(rk.parent_tmp, g.block * 8);
+  AL(rk.scratch, 64 * 8);
+  if (g.C > 1) {
+    AL(rk.recv, (uint64_t)g.C * W * 4);
+    AL(rk.winner, g.block);
+    AL(rk.req, ((uint64_t)g.C * W + 32) * 4);
+    AL(rk.reqin, ((uint64_t)g.C * W + 32) * 4);
+    AL(rk.off_in, ((uint64_t)g.C * W + 32) * 4);
+    AL(rk.off_req, ((uint64_t)g.C * W + 32) * 4);
+    AL(rk.resp, g.nrows() * 4);
+    AL(rk.respin, g.nrows() * 4);
+    rk.scan_tmp_bytes = popc_scan_tmp_bytes((uint64_t)g.C * W);
+    AL(rk.scan_tmp, rk.scan_tmp_bytes);
+    CKR(cudaMemsetAsync(rk.req, 0, ((uint64_t)g.C * W + 32) * 4, G.stream));
+    CKR(cudaMemsetAsync(rk.reqin, 0, ((uint64_t)g.C * W + 32) * 4, G.stream));
+  }
+#undef AL
+  return BFS_OK;
+}
+
+// release every resource held by *G (the Graph object itself is owned by bfs_graph)
+static void release_graph(Graph* G) {
+  if (!G) return;
+  cudaSetDevice(G->device);
+  if (G->stream) cudaStreamSynchronize(G->stream);
+  for (void* p : G->allocs) cudaFree(p);
+  G->allocs.clear();
+  for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
+  G->ev.clear();
+  if (G->h_infos) cudaFreeHost(G->h_infos);
+  if (G->h_scratch) cudaFreeHost(G->h_scratch);
+  if (G->rowc) ncclCommDestroy(G->rowc);
+  if (G->colc) ncclCommDestroy(G->colc);
+  if (G->world) ncclCommDestroy(G->world);
+  if (G->owns_stream && G->stream) cudaStreamDestroy(G->stream);
+  G->stream = nullptr;
+  G->h_infos = nullptr;
+  G->h_scratch = nullptr;
+  G->rowc = G->colc = G->world = nullptr;
+}
+
+static int check_opts(const bfs_opts* o) {
+  if (!o) return BFS_OK;
+  const int E = o->edges_per_thread;
+  if (E != 0 && E != 1 && E != 2 && E != 4 && E != 8 && E != 16)
+    return set_err(BFS_EINVAL, "edges_per_thread must be 1, 2, 4, 8 or 16 (got %d)", E);
+  return BFS_OK;
+}
+
+static void apply_opts(Graph& G, const bfs_opts* o) {
+  bfs_opts d{};
+  if (o) d = *o;
+  if (!d.edges_per_thread) d.edges_per_thread = 4;
+  G.opts = d;
+}
+
+static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uint64_t nverts, int R, int C,
+                  const bfs_comm* comm, const bfs_opts* opts, Graph* Gp) {
+  Graph& G = *Gp;
+  bfs_comm cm{};
+  if (comm) {
+    cm = *comm;
+  } else {
+    cm.loopback = 1;
+    cm.nranks = 1;
+    cudaGetDevice(&cm.device);
+  }
+  const int P = R * C;
+  if (!cm.loopback && P != cm.nranks) return set_err(BFS_EINVAL, "R*C=%d != nranks=%d", P, cm.nranks);
+  if (!cm.loopback && (cm.rank < 0 || cm.rank >= cm.nranks)) return set_err(BFS_EINVAL, "bad rank %d", cm.rank);
+  G.device = cm.device;
+  CKR(cudaSetDevice(G.device));
+  G.loopback = cm.loopback || P == 1;
+  G.world_rank = G.loopback ? 0 : cm.rank;
+  G.world_size = G.loopback ? 1 : cm.nranks;
+  apply_opts(G, opts);
+  if (G.opts.stream) {
+    G.stream = (cudaStream_t)G.opts.stream;
+  } else {
+    CKR(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking));
+    G.owns_stream = true;
+  }
+  // geometry: pad N to a multiple of 32*R*C; ids must fit u32 below the sentinel
+  const uint64_t q = 32ull * (uint64_t)P;
+  G.g.nverts = nverts;
+  G.g.npad = (nverts + q - 1) / q * q;
+  if (G.g.npad >= 0xFFFFFFFFull) return set_err(BFS_EINVAL, "nverts too large: padded %llu >= 2^32", (ull)G.g.npad);
+  G.g.R = R;
+  G.g.C = C;
+  G.g.block = G.g.npad / P;
+  G.ntuples = nedges;
+  CKR(cudaMallocHost(&G.h_scratch, 16 * sizeof(ull)));
+  {
+    int rc = G_alloc(G, (void**)&G.dscratch, 16 * sizeof(ull));
+    if (rc) return rc;
+  }
+  if (!G.loopback) {
+    ncclUniqueId id;
+    memcpy(&id, cm.nccl_id, sizeof id);
+    NKR(ncclCommInitRank(&G.world, cm.nranks, id, cm.rank));
+    const int i = cm.rank % R, j = cm.rank / R;
+    NKR(ncclCommSplit(G.world, i, j, &G.rowc, nullptr));  // grid row i, ordered by column j
+    NKR(ncclCommSplit(G.world, j, i, &G.colc, nullptr));  // grid column j, ordered by row i
+  }
+  const int nlocal = G.loopback ? P : 1;
+  G.ranks.resize(nlocal);
+  for (int k = 0; k < nlocal; ++k) {
+    Rank& rk = G.ranks[k];
+    rk.r = G.loopback ? k : cm.rank;
+    rk.i = rk.r % R;
+    rk.j = rk.r / R;
+  }
+  int rc = build_graph(G, src, dst, nedges);
+  if (rc) return rc;
+  rc = G_alloc(G, (void**)&G.infos, nlocal * sizeof(LevelInfo));
+  if (rc) return rc;
+  CKR(cudaMallocHost(&G.h_infos, nlocal * sizeof(LevelInfo)));
+  for (int k = 0; k < nlocal; ++k) {
+    G.ranks[k].info = G.infos + k;
+    rc = alloc_state(G, G.ranks[k]);
+    if (rc) return rc;
+  }
+  CKR(cudaStreamSynchronize(G.stream));
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ phase events
+static int ev_prepare(Graph& G, int level) {
+  const size_t need = (size_t)(level + 1) * 7;
+  while (G.ev.size() < need) {
+    cudaEvent_t e;
+    CKR(cudaEventCreate(&e));
+    G.ev.push_back(e);
+  }
+  return BFS_OK;
+}
+
+static inline int ev_rec(Graph& G, int level, int p) {
+  if (!G.opts.phase_timing) return BFS_OK;
+  int rc = ev_prepare(G, level);
+  if (rc) return rc;
+  CKR(cudaEventRecord(G.ev[(size_t)level * 7 + p], G.stream));
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ parent resolution (C > 1)
+static int resolve_parents(Graph& G, int64_t* const* par_dev) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  const int C = g.C;
+  cudaStream_t s = G.stream;
+  for (Rank& rk : G.ranks) CKR(launch_req_build(g, rk, s));
+  // requests: rank (i,j) sends req segment c to (i,c), which stores it as reqin segment j
+  if (G.world_size == 1) {
+    for (Rank& dst : G.ranks)
+      for (int c = 0; c < C; ++c) {
+        if (c == dst.j) continue;
+        const Rank& src = G.ranks[c * g.R + dst.i];
+        CKR(cudaMemcpyAsync(dst.reqin + (uint64_t)c * W, src.req + (uint64_t)dst.j * W, W * 4,
+                            cudaMemcpyDeviceToDevice, s));
+      }
+  } else {
+    Rank& rk = G.ranks[0];
+    NKR(ncclGroupStart());
+    for (int c = 0; c < C; ++c) {
+      if (c == rk.j) continue;
+      NKR(ncclSend(rk.req + (uint64_t)c * W, W, ncclUint32, c, G.rowc, s));
+      NKR(ncclRecv(rk.reqin + (uint64_t)c * W, W, ncclUint32, c, G.rowc, s));
+    }
+    NKR(ncclGroupEnd());
+  }
+  // popcount scans of requests received / sent, segment totals to the host
+  const size_t nl = G.ranks.size();
+  std::vector<ull> h_tot(nl * 2 * 64);
+  for (size_t k = 0; k < nl; ++k) {
+    Rank& rk = G.ranks[k];
+    CKR(launch_popc_scan(rk.reqin, rk.off_in, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
+    CKR(launch_popc_scan(rk.req, rk.off_req, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
+    CKR(launch_seg_totals(rk.off_in, W, C, rk.scratch, s));
+    CKR(launch_seg_totals(rk.off_req, W, C, rk.scratch + 64 / 2, s));
+    CKR(launch_resp_pack(g, rk, s));
+    CKR(cudaMemcpyAsync(&h_tot[k * 128], rk.scratch, 64 * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  }
+  CKR(cudaStreamSynchronize(s));
+  // answers: (i,c) sends resp segment j (count = popc(reqin_j)) to (i,j) -> respin segment c
+  if (G.world_size == 1) {
+    for (size_t k = 0; k < nl; ++k) {
+      Rank& dst = G.ranks[k];
+      for (int c = 0; c < C; ++c) {
+        if (c == dst.j) continue;
+        const ull cnt = h_tot[k * 128 + 32 + c];  // popc(req segment c) of the owner
+        if (!cnt) continue;
+        const Rank& src = G.ranks[c * g.R + dst.i];
+        CKR(cudaMemcpyAsync(dst.respin + (uint64_t)c * g.block, src.resp + (uint64_t)dst.j * g.block, cnt * 4,
+                            cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  } else {
+    Rank& rk = G.ranks[0];
+    NKR(ncclGroupStart());
+    for (int c = 0; c < C; ++c) {
+      if (c == rk.j) continue;
+      const ull scnt = h_tot[c], rcnt = h_tot[32 + c];
+      if (scnt) NKR(ncclSend(rk.resp + (uint64_t)c * g.block, scnt, ncclUint32, c, G.rowc, s));
+      if (rcnt) NKR(ncclRecv(rk.respin + (uint64_t)c * g.block, rcnt, ncclUint32, c, G.rowc, s));
+    }
+    NKR(ncclGroupEnd());
+  }
+  for (size_t k = 0; k < nl; ++k) CKR(launch_resp_scatter(g, G.ranks[k], par_dev[k], s));
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ one BFS
+static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
+  const Geom& g = G.g;
+  cudaStream_t s = G.stream;
+  const int E = G.opts.edges_per_thread;
+  const uint32_t tile_edges = (uint32_t)(kExpandThreads * E);
+  const uint64_t W = g.words_block();
+  const uint64_t owner = root / g.block;
+  bool owner_local = false;
+  for (Rank& rk : G.ranks) {
+    owner_local |= (uint64_t)rk.r == owner;
+    CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, s));
+  }
+  G.lvl_frontier.clear();
+  G.lvl_edges.clear();
+  ull bytes = 0;
+  int lvl = 1, nlev = 0;
+  int rc;
+  for (;;) {
+    if (nlev >= kMaxLevels) return set_err(BFS_ESTATE, "level limit exceeded");
+    if ((rc = ev_rec(G, nlev, 0))) return rc;
+    if ((rc = expand_exchange(G))) return rc;
+    if ((rc = ev_rec(G, nlev, 1))) return rc;
+    for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
+    if ((rc = ev_rec(G, nlev, 2))) return rc;
+    for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, s));
+    if ((rc = ev_rec(G, nlev, 3))) return rc;
+    if ((rc = fold_exchange(G))) return rc;
+    if ((rc = ev_rec(G, nlev, 4))) return rc;
+    for (Rank& rk : G.ranks) CKR(launch_update(g, rk, lvl, s));
+    if ((rc = ev_rec(G, nlev, 5))) return rc;
+    if (G.world_size > 1) NKR(ncclAllReduce(&G.infos[0].newv, &G.infos[0].newv, 1, ncclUint64, ncclSum, G.world, s));
+    CKR(cudaMemcpyAsync(G.h_infos, G.infos, G.ranks.size() * sizeof(LevelInfo), cudaMemcpyDeviceToHost, s));
+    if ((rc = ev_rec(G, nlev, 6))) return rc;
+    CKR(cudaStreamSynchronize(s));
+    ull total_new = 0, fr = 0, ed = 0;
+    for (size_t k = 0; k < G.ranks.size(); ++k) {
+      total_new += G.h_infos[k].newv;
+      fr += G.h_infos[k].n;
+      ed += G.h_infos[k].edges;
+    }
+    G.lvl_frontier.push_back(fr);
+    G.lvl_edges.push_back(ed);
+    bytes += (ull)G.ranks.size() * ((ull)(g.R - 1) + (ull)(g.C - 1)) * W * 4;
+    ++nlev;
+    if (total_new == 0) break;
+    ++lvl;
+  }
+  G.last_levels = nlev;
+  // outputs
+  const size_t nl = G.ranks.size();
+  const bool par_is_dev = is_device_ptr(parent), lev_is_dev = is_device_ptr(level);
+  std::vector<int64_t*> par_dev(nl, nullptr);
+  for (size_t k = 0; k < nl; ++k) {
+    Rank& rk = G.ranks[k];
+    par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : rk.parent_tmp;
+    CKR(launch_finalize(g, rk, par_dev[k], (level && lev_is_dev) ? level + k * g.block : nullptr, s));
+  }
+  if (g.C > 1 && parent) {
+    if ((rc = resolve_parents(G, par_dev.data()))) return rc;
+  }
+  for (size_t k = 0; k < nl; ++k) {
+    Rank& rk = G.ranks[k];
+    if (parent && !par_is_dev)
+      CKR(cudaMemcpyAsync(parent + k * g.block, rk.parent_tmp, g.block * 8, cudaMemcpyDeviceToHost, s));
+    if (level && !lev_is_dev)
+      CKR(cudaMemcpyAsync(level + k * g.block, rk.level, g.block * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CKR(cudaStreamSynchronize(s));
+  G.has_run = true;
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    stats->nlevels = nlev;
+    for (int l = 0; l < nlev; ++l) {
+      stats->edges_scanned += G.lvl_edges[l];
+      stats->frontier_columns += G.lvl_frontier[l];
+    }
+    stats->bytes_exchanged = bytes;
+    stats->reached = 0;
+    // own kernels: seed (owner only) + per level and local rank scan(3) + expand + update, then
+    // finalize; with C > 1 the resolution adds req_build, 2 seg_totals, resp_pack, resp_scatter.
+    const uint64_t nl = G.ranks.size();
+    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (5ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
+  }
+  return BFS_OK;
+}
+
+}  // namespace bfs200
+
+using namespace bfs200;
+
+struct bfs_graph {
+  Graph G;
+};
+
+#define ENTER(gp)                                                        \
+  if (!(gp)) return set_err(BFS_EINVAL, "null graph");                   \
+  Graph& G = (gp)->G;                                                    \
+  if (G.broken) return set_err(BFS_ESTATE, "graph unusable after an earlier fatal error"); \
+  if (cudaSetDevice(G.device) != cudaSuccess) return cuda_fail(G, cudaGetLastError(), "cudaSetDevice", __FILE__, __LINE__);
+
+extern "C" {
+
+int bfs_nccl_unique_id(unsigned char* out128) {
+  if (!out128) return set_err(BFS_EINVAL, "null output");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(BFS_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out128, &id, 128);
+  return BFS_OK;
+}
+
+int bfs_graph_create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uint64_t nverts, int R, int C,
+                     const bfs_comm* comm, const bfs_opts* opts, bfs_graph** out) {
+  if (!out) return set_err(BFS_EINVAL, "null out");
+  *out = nullptr;
+  if (nedges && (!src || !dst)) return set_err(BFS_EINVAL, "null edge arrays");
+  if (nverts < 1) return set_err(BFS_EINVAL, "nverts must be >= 1");
+  if (R < 1 || C < 1 || R * C > 64) return set_err(BFS_EINVAL, "grid %dx%d not supported (1 <= R*C <= 64)", R, C);
+  if (C > 32) return set_err(BFS_EINVAL, "C must be <= 32");
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  bfs_graph* gp = nullptr;
+  try {
+    gp = new bfs_graph();
+  } catch (std::bad_alloc&) {
+    return set_err(BFS_ENOMEM, "host allocation failed");
+  }
+  try {
+    rc = create(src, dst, nedges, nverts, R, C, comm, opts, &gp->G);
+  } catch (std::bad_alloc&) {
+    rc = set_err(BFS_ENOMEM, "host allocation failed");
+  }
+  if (rc) {
+    std::string keep = bfs_last_error();
+    release_graph(&gp->G);
+    delete gp;
+    tl_err = keep;
+    return rc;
+  }
+  *out = gp;
+  return BFS_OK;
+}
+
+int bfs_graph_info(const bfs_graph* gp, bfs_info* info) {
+  if (!gp || !info) return set_err(BFS_EINVAL, "null argument");
+  const Graph& G = gp->G;
+  memset(info, 0, sizeof *info);
+  info->nverts = G.g.nverts;
+  info->npad = G.g.npad;
+  info->block = G.g.block;
+  info->R = G.g.R;
+  info->C = G.g.C;
+  info->rank = G.ranks.empty() ? 0 : G.ranks[0].r;
+  info->nlocal = (int)G.ranks.size();
+  info->first_vertex = (uint64_t)info->rank * G.g.block;
+  info->nout = (uint64_t)info->nlocal * G.g.block;
+  for (const Rank& rk : G.ranks) info->nnz_local += rk.nnz;
+  info->ntuples = G.ntuples;
+  info->device_bytes = G.device_bytes;
+  return BFS_OK;
+}
+
+int bfs_set_opts(bfs_graph* gp, const bfs_opts* opts) {
+  ENTER(gp);
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  cudaStream_t old = G.stream;
+  bool owned = G.owns_stream;
+  apply_opts(G, opts);
+  if (G.opts.stream) {
+    if (owned && old != (cudaStream_t)G.opts.stream) {
+      cudaStreamSynchronize(old);
+      cudaStreamDestroy(old);
+    }
+    G.stream = (cudaStream_t)G.opts.stream;
+    G.owns_stream = false;
+  } else {
+    G.opts.stream = owned ? (void*)old : nullptr;
+    if (!owned) {
+      CKR(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking));
+      G.owns_stream = true;
+    }
+  }
+  return BFS_OK;
+}
+
+int bfs_degree(bfs_graph* gp, uint64_t v, uint64_t* degree) {
+  ENTER(gp);
+  if (!degree) return set_err(BFS_EINVAL, "null output");
+  if (v >= G.g.nverts) return set_err(BFS_ERANGE, "vertex %llu >= nverts", (ull)v);
+  const uint64_t jv = v / G.g.ncols(), u = v % G.g.ncols();
+  CKR(cudaMemsetAsync(G.dscratch, 0, sizeof(ull), G.stream));
+  for (Rank& rk : G.ranks)
+    if ((uint64_t)rk.j == jv) CKR(launch_degree(rk, u, G.dscratch, G.stream));
+  if (G.world_size > 1) NKR(ncclAllReduce(G.dscratch, G.dscratch, 1, ncclUint64, ncclSum, G.world, G.stream));
+  CKR(cudaMemcpyAsync(G.h_scratch, G.dscratch, sizeof(ull), cudaMemcpyDeviceToHost, G.stream));
+  CKR(cudaStreamSynchronize(G.stream));
+  *degree = G.h_scratch[0];
+  return BFS_OK;
+}
+
+int bfs_run(bfs_graph* gp, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
+  ENTER(gp);
+  if (root >= G.g.nverts) return set_err(BFS_ERANGE, "root %llu >= nverts %llu", (ull)root, (ull)G.g.nverts);
+  try {
+    return run(G, root, parent, level, stats);
+  } catch (std::bad_alloc&) {
+    return set_err(BFS_ENOMEM, "host allocation failed");
+  }
+}
+
+int bfs_mcomp(bfs_graph* gp, uint64_t* m_comp) {
+  ENTER(gp);
+  if (!m_comp) return set_err(BFS_EINVAL, "null output");
+  if (!G.has_run) return set_err(BFS_ESTATE, "no BFS has run on this graph");
+  CKR(cudaMemsetAsync(G.dscratch, 0, sizeof(ull), G.stream));
+  for (Rank& rk : G.ranks) CKR(launch_mcomp(G.g, rk, G.dscratch, G.stream));
+  if (G.world_size > 1) NKR(ncclAllReduce(G.dscratch, G.dscratch, 1, ncclUint64, ncclSum, G.world, G.stream));
+  CKR(cudaMemcpyAsync(G.h_scratch, G.dscratch, sizeof(ull), cudaMemcpyDeviceToHost, G.stream));
+  CKR(cudaStreamSynchronize(G.stream));
+  *m_comp = G.h_scratch[0];
+  return BFS_OK;
+}
+
+int bfs_level_times(bfs_graph* gp, bfs_level_record* out, int max_levels, int* nlevels) {
+  ENTER(gp);
+  if (!nlevels) return set_err(BFS_EINVAL, "null nlevels");
+  if (!G.has_run) return set_err(BFS_ESTATE, "no BFS has run on this graph");
+  if (!G.opts.phase_timing) return set_err(BFS_ESTATE, "phase_timing was off for the last run");
+  *nlevels = G.last_levels;
+  const int n = G.last_levels < max_levels ? G.last_levels : max_levels;
+  if (n > 0 && !out) return set_err(BFS_EINVAL, "null output");
+  for (int l = 0; l < n; ++l) {
+    float t[6];
+    for (int p = 0; p < 6; ++p) {
+      CKR(cudaEventSynchronize(G.ev[(size_t)l * 7 + p + 1]));
+      CKR(cudaEventElapsedTime(&t[p], G.ev[(size_t)l * 7 + p], G.ev[(size_t)l * 7 + p + 1]));
+    }
+    out[l].expand_comm = t[0];
+    out[l].scan = t[1];
+    out[l].expand = t[2];
+    out[l].fold_comm = t[3];
+    out[l].update = t[4];
+    out[l].allreduce = t[5];
+    out[l].frontier = G.lvl_frontier[l];
+    out[l].edges = G.lvl_edges[l];
+  }
+  return BFS_OK;
+}
+
+void bfs_destroy(bfs_graph* gp) {
+  if (!gp) return;
+  release_graph(&gp->G);
+  delete gp;
+}
+
+const char* bfs_strerror(int status) {
+  switch (status) {
+    case BFS_OK: return "ok";
+    case BFS_EINVAL: return "invalid argument";
+    case BFS_ERANGE: return "vertex id out of range";
+    case BFS_ENOMEM: return "out of memory";
+    case BFS_ECUDA: return "CUDA error";
+    case BFS_ENCCL: return "NCCL error";
+    case BFS_ESTATE: return "graph in unusable state";
+    default: return "unknown status";
+  }
+}
+
+const char* bfs_last_error(void) { return tl_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,39 @@
+// kernels.cuh -- launchers for the hot-path kernels (sm_100a).  See kernels.cu.
+#pragma once
+#include "bfs_internal.h"
+
+namespace bfs200 {
+
+// Alg.2 init lines P:334-343: reset per-search state of one rank and seed the root on its owner.
+cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s);
+
+// K3: frontier bitmap (ncols bits) -> ascending list of columns with degree > 0, their row
+// offsets and the exclusive scan of their degrees.
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s);
+
+// K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
+cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, cudaStream_t s);
+
+// K2: frontier update + pack; lvl is the level being assigned.
+cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s);
+
+// Finalize: parent/level outputs for owned vertices whose parent is local.
+cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s);
+
+// Parent resolution (C > 1): build request bitmaps, answer requests, scatter answers.
+cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s);
+cudaError_t launch_popc_scan(const uint32_t* bits, uint32_t* off, uint64_t nwords, void* tmp, size_t tmp_bytes,
+                             cudaStream_t s);
+size_t popc_scan_tmp_bytes(uint64_t nwords);
+cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s);
+cudaError_t launch_resp_scatter(const Geom& g, Rank& rk, int64_t* parent_out, cudaStream_t s);
+
+cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s);
+
+// m_comp: sum of tdeg over reached owned vertices into *out (device u64).
+cudaError_t launch_mcomp(const Geom& g, Rank& rk, unsigned long long* out, cudaStream_t s);
+
+// Degree of local column u summed into *out (device u64).
+cudaError_t launch_degree(Rank& rk, uint64_t u, unsigned long long* out, cudaStream_t s);
+
+}  // namespace bfs200

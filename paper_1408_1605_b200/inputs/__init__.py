@@ -3,7 +3,7 @@
 This module is the ONE piece shared by the CUDA path's harness and the CPU oracle's tests: it
 generates inputs and holds none of the BFS method's arithmetic.  The generator itself is
 defined once in ``kron_gen.h``; this file loads its host build (``libkron_host.so``).  The
-device build (``csrc/kron_gen.cu``) includes the same header, so both produce identical tuples.
+device build (``kron_dev.cu`` -> ``libkron_dev.so``) includes the same header, so both produce identical tuples.
 
 Workload recipe: scale S, edge factor 16, A,B,C,D = .57,.19,.19,.05, graph
 seed 1, root seed 2, 64 distinct roots uniform over vertices of degree >= 1 (self-loops
@@ -124,3 +124,37 @@ def sample_roots(nverts: int, nroots: int, eligible, root_seed: int = ROOT_SEED,
             if len(roots) == nroots:
                 break
     return roots
+
+
+# ---------------------------------------------------------------- device twin (libkron_dev.so)
+_DEV_LIB = os.path.join(_HERE, "libkron_dev.so")
+_dlib = None
+
+
+def dev_lib():
+    global _dlib
+    if _dlib is None:
+        if not os.path.exists(_DEV_LIB):
+            raise RuntimeError(f"{_DEV_LIB} not built: run __graft_entry__.build()")
+        L = ctypes.CDLL(_DEV_LIB)
+        L.kron_device_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.kron_device_generate.restype = ctypes.c_int
+        _dlib = L
+    return _dlib
+
+
+def generate_device(scale: int, edgefactor: int = EDGE_FACTOR, seed: int = GRAPH_SEED, k0: int = 0, count=None,
+                    device="cuda"):
+    """Tuples [k0, k0+count) generated directly in HBM: two torch uint64 CUDA tensors."""
+    import torch
+    if count is None:
+        count = num_tuples(scale, edgefactor) - k0
+    s = torch.empty(int(count), dtype=torch.uint64, device=device)
+    d = torch.empty(int(count), dtype=torch.uint64, device=device)
+    stream = torch.cuda.current_stream(s.device).cuda_stream
+    rc = dev_lib().kron_device_generate(int(scale), int(seed), int(k0), int(count), s.data_ptr(), d.data_ptr(),
+                                        stream)
+    if rc != 0:
+        raise RuntimeError(f"kron_device_generate failed: cudaError {rc}")
+    return s, d

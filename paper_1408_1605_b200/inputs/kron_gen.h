@@ -3,7 +3,7 @@
  *
  * This header is the single definition of the benchmark input.  It is shared by the
  * host generator (inputs/kron_host.c, used by tests and the CPU oracle leg) and the
- * device generator (csrc/kron_gen.cu, used by bench.py), so both produce bit-identical
+ * device generator (inputs/kron_dev.cu, used by bench.py), so both produce bit-identical
  * tuple lists.  It holds NONE of the BFS method's arithmetic: no partitioning, no CSC,
  * no traversal.  (The oracle never includes it; it receives plain edge arrays.)
  *

@@ -1,7 +1,7 @@
 /*
  * kron_host.c -- host twin of the seeded Kronecker input generator (definition in kron_gen.h).
  * Input generation only: no BFS arithmetic.  Built as libkron_host.so; used by the tests and
- * by the CPU-oracle leg of bench.py.  Bit-identical to the device generator (csrc/kron_gen.cu).
+ * by the CPU-oracle leg of bench.py.  Bit-identical to the device generator (inputs/kron_dev.cu).
  */
 #include "kron_gen.h"
 #include <stddef.h>
