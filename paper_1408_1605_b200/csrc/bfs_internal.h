@@ -13,8 +13,8 @@
 namespace bfs200 {
 
 constexpr uint32_t kNoPred = 0xFFFFFFFFu;  // "no candidate" sentinel in pred[] (R11)
-constexpr int kScanTileWords = 2048;       // bitmap words per unpack/scan tile (65536 vertices)
-constexpr int kScanThreads = 256;          // 8 words per thread
+constexpr int kScanSegWords = 256;         // bitmap words per warp segment of the unpack/scan (8192 vertices)
+constexpr int kScanThreads = 256;          // 8 warps = 8 segments per CTA
 constexpr int kExpandThreads = 256;
 constexpr int kMaxLevels = 4096;
 
@@ -24,7 +24,8 @@ struct LevelInfo {
   unsigned long long n;      // frontier columns with local degree > 0
   unsigned long long edges;  // cumul[n]
   unsigned long long newv;   // vertices discovered by the update (this rank)
-  unsigned long long pad;
+  unsigned long long mode;   // parent claim of this level: 1 = atomicMin in the expansion (P1),
+                             // 2 = CSR scan of the discovered rows (P2); see k_scan_segs
 };
 
 // Geometry of the 2D partition (index maps SPEC.md S:109-148).
@@ -42,25 +43,34 @@ struct Rank {
   uint64_t nnz = 0;   // CSC entries
   unsigned long long* col = nullptr;  // [ncols+1] column offsets (u64: nnz can exceed 2^32)
   uint32_t* row = nullptr;    // [nnz] local row ids, ascending within each column
+  // CSR view of the same local matrix (row -> ascending local columns) for the parent pass;
+  // with R = C = 1 the matrix is symmetric and these alias col/row.
+  unsigned long long* csr_ptr = nullptr;  // [nrows+1]
+  uint32_t* csr_col = nullptr;            // [nnz]
   uint32_t* tdeg = nullptr;   // [block] input tuples whose source is the owned vertex (m_comp)
   // per-search state
-  uint32_t* visited = nullptr;   // [nrows/32] visited bitmap over ALL local rows
-  uint32_t* disc = nullptr;      // [nrows/32] rows discovered in this level, C segments of block bits
+  // visited bitmap over ALL local rows interleaved word by word with the
+  // rows discovered in the current level: vd[2w] = visited word w, vd[2w+1] = discovered word w,
+  // so the expansion tests both with one 8-byte load.
+  uint32_t* vd = nullptr;        // [2 * nrows/32]
+  uint32_t* sendbuf = nullptr;   // [nrows/32] discovered rows packed contiguously (fold message, C>1)
   uint32_t* recv = nullptr;      // [C * block/32] fold receive buffer (segment c from P_ic); C>1 only
   uint32_t* all_front = nullptr; // [ncols/32] gathered frontier bitmap; own segment i = own frontier
   uint32_t* pred = nullptr;      // [nrows] min parent candidate (global id) per local row
+  uint32_t* pmin = nullptr;      // [nrows] atomicMin scratch of P1 levels; all UINT32_MAX between levels
   int32_t* level = nullptr;      // [block] owned levels
   uint8_t* winner = nullptr;     // [block] grid column that supplied the parent (C>1 only)
   uint32_t* flist = nullptr;     // [ncols] frontier columns with degree>0, ascending
   unsigned long long* rowoff = nullptr;  // [ncols] col[flist[k]]
   unsigned long long* cumul = nullptr;   // [ncols+1] exclusive scan of degrees
   uint32_t* tile_k = nullptr;            // [nnz/256 + 2] first frontier index of every expansion tile
-  uint32_t* tile_cnt = nullptr;          // [ntiles] per-tile frontier count
-  unsigned long long* tile_sum = nullptr;// [ntiles] per-tile degree sum
-  uint32_t* tile_cnt_off = nullptr;
-  unsigned long long* tile_sum_off = nullptr;
+  uint32_t* seg_cnt = nullptr;           // [nseg] per-segment frontier count (degree > 0)
+  unsigned long long* seg_sum = nullptr; // [nseg] per-segment degree sum
+  uint32_t* seg_cnt_off = nullptr;       // exclusive scans of the above
+  unsigned long long* seg_sum_off = nullptr;
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution
+  int32_t* level_tmp = nullptr;          // [block] level staging for host outputs
   // parent resolution (C>1)
   uint32_t* req = nullptr;       // [C * block/32] request bitmaps: rows whose parent lives at P_ic
   uint32_t* reqin = nullptr;     // [C * block/32] requests received from P_ic (rows of segment c)

@@ -100,6 +100,15 @@ __global__ void k_keys_to_rows(const ull* keys, uint64_t n, ull rmask, uint32_t*
     row[t] = (uint32_t)(keys[t] & rmask);
 }
 
+// CSC key (col << rbits | row) -> CSR key (row << cbits | col)
+__global__ void k_swap_keys(ull* keys, uint64_t n, int rbits, int cbits) {
+  const ull rmask = (1ull << rbits) - 1;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    const ull k = keys[t];
+    keys[t] = ((k & rmask) << cbits) | (k >> rbits);
+  }
+}
+
 // col[c] = first position with key >= c << rbits (lower bound), c in [0, ncols]
 __global__ void k_col_offsets(const ull* keys, uint64_t n, int rbits, uint64_t ncols, ull* col) {
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= ncols;
@@ -160,6 +169,33 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits) {
   }
   const uint64_t nc = g.ncols() + 1;
   k_col_offsets<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(keys, rk.nnz, rbits, g.ncols(), rk.col);
+  CKR(cudaGetLastError());
+  CKR(cudaStreamSynchronize(s));
+  // CSR of the same local matrix for the parent pass (rows scanned in ascending column order).
+  // With a 1x1 grid the matrix is the symmetric adjacency, so the CSC already is its CSR.
+  if (g.R * g.C == 1) {
+    rk.csr_ptr = rk.col;
+    rk.csr_col = rk.row;
+    return BFS_OK;
+  }
+  const int cbits = bits_for(g.ncols());
+  rc = G_alloc(G, (void**)&rk.csr_col, (rk.nnz ? rk.nnz : 1) * sizeof(uint32_t));
+  if (rc) return rc;
+  rc = G_alloc(G, (void**)&rk.csr_ptr, (g.nrows() + 1) * sizeof(ull));
+  if (rc) return rc;
+  if (rk.nnz) {
+    k_swap_keys<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, cbits);
+    CKR(cudaGetLastError());
+    tmp_bytes = 0;
+    CKR(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys, (uint64_t)rk.nnz, 0, rbits + cbits, s));
+    CKR(sc.alloc(&sorted, rk.nnz * sizeof(ull)));
+    CKR(sc.alloc(&tmp, tmp_bytes));
+    CKR(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (uint64_t)rk.nnz, 0, rbits + cbits, s));
+    k_keys_to_rows<<<4096, 256, 0, s>>>(sorted, rk.nnz, (1ull << cbits) - 1, rk.csr_col);
+    CKR(cudaGetLastError());
+  }
+  const uint64_t nr = g.nrows() + 1;
+  k_col_offsets<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(sorted, rk.nnz, cbits, g.nrows(), rk.csr_ptr);
   CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
   return BFS_OK;

@@ -148,7 +148,7 @@ static int fold_exchange(Graph& G) {
       for (int c = 0; c < g.C; ++c) {
         if (c == dst.j) continue;
         const Rank& src = G.ranks[c * g.R + dst.i];
-        CKR(cudaMemcpyAsync(dst.recv + c * W, src.disc + (uint64_t)dst.j * W, W * 4, cudaMemcpyDeviceToDevice,
+        CKR(cudaMemcpyAsync(dst.recv + c * W, src.sendbuf + (uint64_t)dst.j * W, W * 4, cudaMemcpyDeviceToDevice,
                             G.stream));
       }
   } else {
@@ -156,7 +156,7 @@ static int fold_exchange(Graph& G) {
     NKR(ncclGroupStart());
     for (int c = 0; c < g.C; ++c) {
       if (c == rk.j) continue;
-      NKR(ncclSend(rk.disc + (uint64_t)c * W, W, ncclUint32, c, G.rowc, G.stream));
+      NKR(ncclSend(rk.sendbuf + (uint64_t)c * W, W, ncclUint32, c, G.rowc, G.stream));
       NKR(ncclRecv(rk.recv + (uint64_t)c * W, W, ncclUint32, c, G.rowc, G.stream));
     }
     NKR(ncclGroupEnd());
@@ -169,27 +169,30 @@ static int alloc_state(Graph& G, Rank& rk) {
   const Geom& g = G.g;
   const uint64_t W = g.words_block();
   const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
-  const uint64_t ntiles = (cw + kScanTileWords - 1) / kScanTileWords;
+  const uint64_t nseg = (cw + kScanSegWords - 1) / kScanSegWords;
   int rc;
 #define AL(ptr, bytes)                                  \
   if ((rc = G_alloc(G, (void**)&(ptr), (bytes))) != 0) \
     return rc;
-  AL(rk.visited, rw * 4);
-  AL(rk.disc, rw * 4);
+  AL(rk.vd, 2 * rw * 4);
   AL(rk.all_front, cw * 4);
   AL(rk.pred, g.nrows() * 4);
+  AL(rk.pmin, g.nrows() * 4);
+  CKR(cudaMemsetAsync(rk.pmin, 0xFF, g.nrows() * 4, G.stream));
   AL(rk.level, g.block * 4);
   AL(rk.flist, g.ncols() * 4);
   AL(rk.rowoff, g.ncols() * 8);
   AL(rk.cumul, (g.ncols() + 1) * 8);
   AL(rk.tile_k, (rk.nnz / 256 + 2) * 4);
-  AL(rk.tile_cnt, ntiles * 4);
-  AL(rk.tile_sum, ntiles * 8);
-  AL(rk.tile_cnt_off, ntiles * 4);
-  AL(rk.tile_sum_off, ntiles * 8);
+  AL(rk.seg_cnt, nseg * 4);
+  AL(rk.seg_sum, nseg * 8);
+  AL(rk.seg_cnt_off, nseg * 4);
+  AL(rk.seg_sum_off, nseg * 8);
   AL(rk.parent_tmp, g.block * 8);
+  AL(rk.level_tmp, g.block * 4);
   AL(rk.scratch, 64 * 8);
   if (g.C > 1) {
+    AL(rk.sendbuf, rw * 4);
     AL(rk.recv, (uint64_t)g.C * W * 4);
     AL(rk.winner, g.block);
     AL(rk.req, ((uint64_t)g.C * W + 32) * 4);
@@ -425,6 +428,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
     if ((rc = ev_rec(G, nlev, 2))) return rc;
     for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, s));
+    for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
     if ((rc = ev_rec(G, nlev, 3))) return rc;
     if ((rc = fold_exchange(G))) return rc;
     if ((rc = ev_rec(G, nlev, 4))) return rc;
@@ -455,7 +459,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : rk.parent_tmp;
-    CKR(launch_finalize(g, rk, par_dev[k], (level && lev_is_dev) ? level + k * g.block : nullptr, s));
+    CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr, s));
   }
   if (g.C > 1 && parent) {
     if ((rc = resolve_parents(G, par_dev.data()))) return rc;
@@ -465,7 +469,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     if (parent && !par_is_dev)
       CKR(cudaMemcpyAsync(parent + k * g.block, rk.parent_tmp, g.block * 8, cudaMemcpyDeviceToHost, s));
     if (level && !lev_is_dev)
-      CKR(cudaMemcpyAsync(level + k * g.block, rk.level, g.block * 4, cudaMemcpyDeviceToHost, s));
+      CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDeviceToHost, s));
   }
   CKR(cudaStreamSynchronize(s));
   G.has_run = true;
@@ -478,10 +482,11 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
     stats->bytes_exchanged = bytes;
     stats->reached = 0;
-    // own kernels: seed (owner only) + per level and local rank scan(3) + expand + update, then
-    // finalize; with C > 1 the resolution adds req_build, 2 seg_totals, resp_pack, resp_scatter.
+    // own kernels: seed (owner only) + per level and local rank scan(3) + expand + parent +
+    // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals,
+    // resp_pack, resp_scatter.
     const uint64_t nl = G.ranks.size();
-    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (5ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
+    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (6ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
   }
   return BFS_OK;
 }

@@ -1,13 +1,16 @@
 // kernels.cu -- hot-path kernels of libbfs200 for sm_100a (B200).
 //
 // Per BFS level on rank P_ij (Alg.2):
-//   K3 k_scan_count / k_scan_tiles / k_scan_emit : frontier bitmap -> ascending column list,
-//        row offsets, exclusive degree scan `cumul` and the per-tile
-//        first-vertex table used to map threads to edges (Fig. t2d_map).
+//   K3 k_scan_count / k_scan_segs / k_scan_emit : frontier bitmap -> ascending list of frontier
+//        columns with local degree > 0, their row offsets, the exclusive degree scan `cumul`
+//         and the per-tile first-column table that maps threads to edges
+//        (Fig. t2d_map).  Warp-cooperative bitmap unpack.
 //   K1 k_expand<E> : one thread per E consecutive frontier edges; the
-//        visited-bitmap filter (Alg.3 lines 5-6); the parent claim by atomicMin of the global
-//        id (deterministic minimum rule, R1) and the discovered-row bitmap by atomicOr
-//        (Alg.3 line 7, bitmap pack fused: P:900-903).
+//        visited filter (Alg.3 lines 5-6) and the discovered-row bitmap by atomicOr (Alg.3 line
+//        7; bitmap pack fused).
+//   K4 k_parent : parent claim for every row discovered in this level: the minimum frontier
+//        column adjacent to it (ascending CSR row scan, first frontier member) -- the
+//        deterministic form of Alg.3 line 17 (R1), without per-edge atomics.
 //   K2 k_update : OR of the received fold segments, new = OR & ~visited, level, visited,
 //        next frontier bitmap, lowest-column winner.
 // All hot-path arithmetic is integer.
@@ -29,243 +32,21 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ void load8(const uint32_t* __restrict__ bm, uint64_t w0, uint64_t nwords, uint32_t (&x)[8]) {
-  if (w0 + 8 <= nwords) {
-    const uint4* p = reinterpret_cast<const uint4*>(bm + w0);
-    uint4 a = __ldg(p), b = __ldg(p + 1);
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) x[q] = (w0 + q < nwords) ? __ldg(bm + w0 + q) : 0u;
-  }
+// visited|discovered pair, cached in L2 only (the discovered word changes during the kernel)
+__device__ __forceinline__ uint2 ld_cg_u2(const uint32_t* p) {
+  uint2 v;
+  asm volatile("ld.global.cg.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
 }
 
-// ------------------------------------------------------------------ init (Alg.2 lines 1-10)
-__global__ void k_seed_root(uint32_t* visited, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
-                            uint64_t t, uint64_t row_local, uint64_t col_local, uint32_t root, int j) {
-  visited[row_local >> 5] |= 1u << (row_local & 31);  // bmap[LOCAL_ROW(r)] <- 1
-  all_front[col_local >> 5] |= 1u << (col_local & 31);  // front[0] <- LOCAL_COL(r)
-  level[t] = 0;                                          // level[LOCAL_ROW(r)] <- 0
-  pred[row_local] = root;                                // pred[LOCAL_ROW(r)] <- r
-  if (winner) winner[t] = (uint8_t)j;
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t m) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(m) : "memory");
 }
 
-cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s) {
-  const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
-  cudaMemsetAsync(rk.visited, 0, rw * 4, s);
-  cudaMemsetAsync(rk.disc, 0, rw * 4, s);
-  cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
-  cudaMemsetAsync(rk.pred, 0xFF, g.nrows() * 4, s);
-  cudaMemsetAsync(rk.level, 0xFF, g.block * 4, s);
-  if (owner) {
-    const uint64_t t = root - (uint64_t)rk.r * g.block;
-    k_seed_root<<<1, 1, 0, s>>>(rk.visited, rk.all_front, rk.level, rk.pred, rk.winner, t,
-                                (uint64_t)rk.j * g.block + t, (uint64_t)rk.i * g.block + t, (uint32_t)root, rk.j);
-  }
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ K3: unpack + degree scan
-struct CS {
-  unsigned int c;
-  ull s;
-};
-struct CSAdd {
-  __device__ __forceinline__ CS operator()(const CS& a, const CS& b) const { return CS{a.c + b.c, a.s + b.s}; }
-};
-
-// per tile of kScanTileWords words: number of frontier columns with degree > 0 and their degree sum
-__global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
-                                                              const ull* __restrict__ col, uint32_t* tile_cnt,
-                                                              ull* tile_sum) {
-  typedef cub::BlockReduce<CS, kScanThreads> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const uint64_t w0 = (uint64_t)blockIdx.x * kScanTileWords + threadIdx.x * 8;
-  uint32_t x[8];
-  load8(bm, w0, nwords, x);
-  CS acc{0u, 0ull};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t b = x[q];
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      const uint64_t u = (w0 + q) * 32 + bit;
-      const ull d = __ldg(col + u + 1) - __ldg(col + u);
-      acc.c += d ? 1u : 0u;
-      acc.s += d;
-    }
-  }
-  CS tot = BR(tmp).Reduce(acc, CSAdd());
-  if (threadIdx.x == 0) {
-    tile_cnt[blockIdx.x] = tot.c;
-    tile_sum[blockIdx.x] = tot.s;
-  }
-}
-
-// exclusive scan over tiles (one CTA); writes n, edges, cumul[n]; resets the update counter
-__global__ void __launch_bounds__(1024) k_scan_tiles(int ntiles, const uint32_t* tile_cnt, const ull* tile_sum,
-                                                     uint32_t* cnt_off, ull* sum_off, LevelInfo* info, ull* cumul) {
-  typedef cub::BlockScan<CS, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ CS carry;
-  if (threadIdx.x == 0) carry = CS{0u, 0ull};
-  __syncthreads();
-  for (int base = 0; base < ntiles; base += 1024) {
-    const int t = base + threadIdx.x;
-    CS v = (t < ntiles) ? CS{tile_cnt[t], tile_sum[t]} : CS{0u, 0ull};
-    CS ex, agg;
-    BS(tmp).ExclusiveScan(v, ex, CS{0u, 0ull}, CSAdd(), agg);
-    const CS c0 = carry;
-    if (t < ntiles) {
-      cnt_off[t] = c0.c + ex.c;
-      sum_off[t] = c0.s + ex.s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry = CS{c0.c + agg.c, c0.s + agg.s};
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    info->n = carry.c;
-    info->edges = carry.s;
-    info->newv = 0;
-    cumul[carry.c] = carry.s;
-  }
-}
-
-// emit the list, row offsets, cumul and, for every expansion tile starting inside a column's
-// edge range, the index of that column (tile_k): the thread->edge mapping table.
-__global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
-                                                             const ull* __restrict__ col, const uint32_t* cnt_off,
-                                                             const ull* sum_off, uint32_t* flist, ull* rowoff,
-                                                             ull* cumul, uint32_t* tile_k, uint32_t tile_edges) {
-  typedef cub::BlockScan<CS, kScanThreads> BS;
-  __shared__ typename BS::TempStorage tmp;
-  const uint64_t w0 = (uint64_t)blockIdx.x * kScanTileWords + threadIdx.x * 8;
-  uint32_t x[8];
-  load8(bm, w0, nwords, x);
-  CS acc{0u, 0ull};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t b = x[q];
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      const uint64_t u = (w0 + q) * 32 + bit;
-      const ull d = __ldg(col + u + 1) - __ldg(col + u);
-      acc.c += d ? 1u : 0u;
-      acc.s += d;
-    }
-  }
-  CS ex;
-  BS(tmp).ExclusiveScan(acc, ex, CS{0u, 0ull}, CSAdd());
-  uint64_t k = cnt_off[blockIdx.x] + ex.c;
-  ull e = sum_off[blockIdx.x] + ex.s;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t b = x[q];
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      const uint64_t u = (w0 + q) * 32 + bit;
-      const ull c0 = __ldg(col + u), d = __ldg(col + u + 1) - c0;
-      if (!d) continue;
-      flist[k] = (uint32_t)u;
-      rowoff[k] = c0;
-      cumul[k] = e;
-      // tiles whose first edge lies in [e, e+d)
-      for (ull t = (e + tile_edges - 1) / tile_edges; t * tile_edges < e + d; ++t) tile_k[t] = (uint32_t)k;
-      ++k;
-      e += d;
-    }
-  }
-}
-
-cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s) {
-  const uint64_t nwords = g.ncols() / 32;
-  const int ntiles = (int)((nwords + kScanTileWords - 1) / kScanTileWords);
-  k_scan_count<<<ntiles, kScanThreads, 0, s>>>(rk.all_front, nwords, rk.col, rk.tile_cnt, rk.tile_sum);
-  k_scan_tiles<<<1, 1024, 0, s>>>(ntiles, rk.tile_cnt, rk.tile_sum, rk.tile_cnt_off, rk.tile_sum_off, rk.info,
-                                  rk.cumul);
-  k_scan_emit<<<ntiles, kScanThreads, 0, s>>>(rk.all_front, nwords, rk.col, rk.tile_cnt_off, rk.tile_sum_off,
-                                              rk.flist, rk.rowoff, rk.cumul, rk.tile_k, tile_edges);
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ K1: frontier expansion
-// Tile of TILE = 256*E consecutive frontier edges per CTA iteration (grid-stride over tiles,
-// persistent grid sized from the SM count).  The tile's columns (<= TILE+1) are staged in
-// shared memory (edge begin within the tile, row offset, column id); each thread maps its
-// first edge by binary search in shared memory and the next E-1 by linear advance.
-template <int E>
-__global__ void __launch_bounds__(kExpandThreads) k_expand(const uint32_t* __restrict__ row,
-                                                           const uint32_t* __restrict__ flist,
-                                                           const ull* __restrict__ rowoff,
-                                                           const ull* __restrict__ cumul,
-                                                           const uint32_t* __restrict__ tile_k,
-                                                           const LevelInfo* __restrict__ info,
-                                                           const uint32_t* __restrict__ visited, uint32_t* pred,
-                                                           uint32_t* disc, uint32_t col_base) {
-  constexpr int TILE = kExpandThreads * E;
-  extern __shared__ __align__(16) unsigned char smem[];
-  ull* s_off = reinterpret_cast<ull*>(smem);               // [TILE+2]
-  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_off + TILE + 2);  // [TILE+2]
-  uint32_t* s_u = s_beg + TILE + 2;                         // [TILE+2]
-  const ull n = info->n, total = info->edges;
-  if (total == 0) return;
-  const ull ntiles = (total + TILE - 1) / TILE;
-  for (ull tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const ull t0 = tile * TILE;
-    const uint32_t len = (uint32_t)min((ull)TILE, total - t0);
-    const uint32_t klo = tile_k[tile];
-    const uint32_t khi = (tile + 1 < ntiles) ? tile_k[tile + 1] : (uint32_t)(n - 1);
-    const uint32_t cnt = khi - klo + 1;
-    for (uint32_t idx = threadIdx.x; idx < cnt; idx += kExpandThreads) {
-      const ull c = cumul[klo + idx];
-      const uint32_t beg = c > t0 ? (uint32_t)(c - t0) : 0u;
-      s_beg[idx] = beg;
-      s_off[idx] = rowoff[klo + idx] + (t0 + beg - c);
-      s_u[idx] = flist[klo + idx];
-    }
-    if (threadIdx.x == 0) s_beg[cnt] = 0xFFFFFFFFu;
-    __syncthreads();
-    const uint32_t le = threadIdx.x * E;
-    if (le < len) {
-      // greatest idx < cnt with s_beg[idx] <= le (binsearch_maxle, Alg.3 line 2)
-      uint32_t lo = 0, hi = cnt - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (s_beg[mid] <= le) lo = mid; else hi = mid - 1;
-      }
-      uint32_t idx = lo;
-      uint32_t v[E], u[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const uint32_t e = le + q;
-        if (e < len) {
-          while (s_beg[idx + 1] <= e) ++idx;  // linear advance
-          v[q] = ld_stream_u32(row + s_off[idx] + (e - s_beg[idx]));  // Alg.3 line 4
-          u[q] = s_u[idx];
-        } else {
-          v[q] = 0xFFFFFFFFu;
-        }
-      }
-      uint32_t w[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) w[q] = (v[q] != 0xFFFFFFFFu) ? __ldg(visited + (v[q] >> 5)) : 0xFFFFFFFFu;
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        if (v[q] == 0xFFFFFFFFu) continue;
-        const uint32_t m = 1u << (v[q] & 31);
-        if (w[q] & m) continue;  // already visited (Alg.3 lines 5-6)
-        const uint32_t ug = col_base + u[q];
-        if (ug < *(volatile uint32_t*)(pred + v[q])) atomicMin(pred + v[q], ug);  // parent claim
-        atomicOr(disc + (v[q] >> 5), m);                                          // discovered row
-      }
-    }
-    __syncthreads();
-  }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
 static int g_num_sms = 0;
@@ -279,6 +60,253 @@ static int num_sms() {
   return g_num_sms;
 }
 
+// ------------------------------------------------------------------ init (Alg.2 lines 1-10)
+__global__ void k_seed_root(uint32_t* vd, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
+                            uint64_t t, uint64_t row_local, uint64_t col_local, uint32_t root, int j) {
+  vd[2 * (row_local >> 5)] |= 1u << (row_local & 31);   // bmap[LOCAL_ROW(r)] <- 1
+  all_front[col_local >> 5] |= 1u << (col_local & 31);  // front[0] <- LOCAL_COL(r)
+  level[t] = 0;                                          // level[LOCAL_ROW(r)] <- 0
+  pred[row_local] = root;                                // pred[LOCAL_ROW(r)] <- r
+  if (winner) winner[t] = (uint8_t)j;
+}
+
+// level[] and pred[] need no reset: both are written for a vertex when it is reached, and every
+// reader masks with the visited bit (unreached -> -1).
+cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s) {
+  const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
+  cudaMemsetAsync(rk.vd, 0, 2 * rw * 4, s);
+  cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
+  if (owner) {
+    const uint64_t t = root - (uint64_t)rk.r * g.block;
+    k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, t, (uint64_t)rk.j * g.block + t,
+                                (uint64_t)rk.i * g.block + t, (uint32_t)root, rk.j);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3: unpack + degree scan
+// A warp owns a segment of kScanSegWords bitmap words; it walks the non-zero words 32 at a
+// time and, per word, lane b handles bit b, so the col[] reads of one word are coalesced.
+__global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
+                                                              uint64_t nseg, const ull* __restrict__ col,
+                                                              uint32_t* seg_cnt, ull* seg_sum) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const uint64_t w0 = seg * kScanSegWords;
+  const uint64_t w1 = min(w0 + kScanSegWords, nwords);
+  unsigned cnt = 0;
+  ull sum = 0;
+  for (uint64_t wb = w0; wb < w1; wb += 32) {
+    const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
+    unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
+    while (nz) {
+      const int jw = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
+      if ((xw >> lane) & 1u) {
+        const uint64_t u = (wb + jw) * 32 + lane;
+        const ull d = __ldg(col + u + 1) - __ldg(col + u);
+        cnt += d ? 1u : 0u;
+        sum += d;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  }
+  if (lane == 0) {
+    seg_cnt[seg] = cnt;
+    seg_sum[seg] = sum;
+  }
+}
+
+struct CS {
+  unsigned int c;
+  ull s;
+};
+struct CSAdd {
+  __device__ __forceinline__ CS operator()(const CS& a, const CS& b) const { return CS{a.c + b.c, a.s + b.s}; }
+};
+
+// exclusive scan over segments (one CTA); writes n, edges, cumul[n]; resets the update counter
+__global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const uint32_t* seg_cnt, const ull* seg_sum,
+                                                    uint32_t* cnt_off, ull* sum_off, LevelInfo* info, ull* cumul,
+                                                    ull nnz) {
+  typedef cub::BlockScan<CS, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ CS carry;
+  if (threadIdx.x == 0) carry = CS{0u, 0ull};
+  __syncthreads();
+  for (uint64_t base = 0; base < nseg; base += 1024) {
+    const uint64_t t = base + threadIdx.x;
+    CS v = (t < nseg) ? CS{seg_cnt[t], seg_sum[t]} : CS{0u, 0ull};
+    CS ex, agg;
+    BS(tmp).ExclusiveScan(v, ex, CS{0u, 0ull}, CSAdd(), agg);
+    const CS c0 = carry;
+    if (t < nseg) {
+      cnt_off[t] = c0.c + ex.c;
+      sum_off[t] = c0.s + ex.s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = CS{c0.c + agg.c, c0.s + agg.s};
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    info->n = carry.c;
+    info->edges = carry.s;
+    info->newv = 0;
+    // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
+    // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
+    // the scan (P2) is used when that is <= 32; otherwise (small frontiers, e.g. the first
+    // levels) the expansion does compare-then-atomicMin per candidate edge (P1).
+    info->mode = (carry.s * 32ull >= nnz) ? 2ull : 1ull;
+    cumul[carry.c] = carry.s;
+  }
+}
+
+// emit the frontier list (columns with degree > 0, ascending), their row offsets, the
+// exclusive degree scan cumul, and for every expansion tile starting inside a column's edge
+// range the index of that column (tile_k): the thread->edge mapping table.
+__global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
+                                                             uint64_t nseg, const ull* __restrict__ col,
+                                                             const uint32_t* cnt_off, const ull* sum_off,
+                                                             uint32_t* flist, ull* rowoff, ull* cumul,
+                                                             uint32_t* tile_k, uint32_t tile_edges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const uint64_t w0 = seg * kScanSegWords;
+  const uint64_t w1 = min(w0 + kScanSegWords, nwords);
+  uint64_t k = cnt_off[seg];
+  ull e = sum_off[seg];
+  const unsigned lt = lanemask_lt();
+  for (uint64_t wb = w0; wb < w1; wb += 32) {
+    const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
+    unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
+    while (nz) {
+      const int jw = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
+      const uint64_t u = (wb + jw) * 32 + lane;
+      ull c0 = 0, d = 0;
+      if ((xw >> lane) & 1u) {
+        c0 = __ldg(col + u);
+        d = __ldg(col + u + 1) - c0;
+      }
+      const unsigned mask = __ballot_sync(0xFFFFFFFFu, d != 0);
+      ull inc = d;  // inclusive warp scan of degrees
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (d) {
+        const uint64_t pos = k + __popc(mask & lt);
+        const ull eb = e + inc - d;
+        flist[pos] = (uint32_t)u;
+        rowoff[pos] = c0;
+        cumul[pos] = eb;
+        for (ull t = (eb + tile_edges - 1) / tile_edges; t * tile_edges < eb + d; ++t) tile_k[t] = (uint32_t)pos;
+      }
+      k += __popc(mask);
+      e += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+  }
+}
+
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s) {
+  const uint64_t nwords = g.ncols() / 32;
+  const uint64_t nseg = (nwords + kScanSegWords - 1) / kScanSegWords;
+  const unsigned grid = (unsigned)((nseg + kScanThreads / 32 - 1) / (kScanThreads / 32));
+  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt, rk.seg_sum);
+  k_scan_segs<<<1, 1024, 0, s>>>(nseg, rk.seg_cnt, rk.seg_sum, rk.seg_cnt_off, rk.seg_sum_off, rk.info, rk.cumul,
+                                 (ull)rk.nnz);
+  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt_off, rk.seg_sum_off,
+                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, tile_edges);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K1: frontier expansion
+// Tile of TILE = 256*E consecutive frontier edges per CTA iteration (grid-stride over tiles,
+// persistent grid sized from the SM count).  The tile's columns (<= TILE+1) are staged in
+// shared memory (edge begin within the tile, row offset); each thread maps its first edge by
+// binary search in shared memory and the next E-1 by linear advance.  The E row
+// loads are issued together, then the E visited|discovered probes (one 8-byte load each),
+// then one RED.OR per edge whose row is neither visited nor already discovered.
+template <int E>
+__global__ void __launch_bounds__(kExpandThreads) k_expand(const uint32_t* __restrict__ row,
+                                                           const uint32_t* __restrict__ flist,
+                                                           const ull* __restrict__ rowoff,
+                                                           const ull* __restrict__ cumul,
+                                                           const uint32_t* __restrict__ tile_k,
+                                                           const LevelInfo* __restrict__ info, uint32_t* vd,
+                                                           uint32_t* pmin, uint32_t col_base) {
+  constexpr int TILE = kExpandThreads * E;
+  extern __shared__ __align__(16) unsigned char smem[];
+  ull* s_off = reinterpret_cast<ull*>(smem);                        // [TILE+2]
+  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_off + TILE + 2);  // [TILE+2]
+  uint32_t* s_u = s_beg + TILE + 2;                                 // [TILE+2]
+  const ull n = info->n, total = info->edges;
+  if (total == 0) return;
+  const bool p1 = info->mode == 1;
+  const ull ntiles = (total + TILE - 1) / TILE;
+  for (ull tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const ull t0 = tile * TILE;
+    const uint32_t len = (uint32_t)min((ull)TILE, total - t0);
+    const uint32_t klo = tile_k[tile];
+    const uint32_t khi = (tile + 1 < ntiles) ? tile_k[tile + 1] : (uint32_t)(n - 1);
+    const uint32_t cnt = khi - klo + 1;
+    for (uint32_t idx = threadIdx.x; idx < cnt; idx += kExpandThreads) {
+      const ull c = cumul[klo + idx];
+      const uint32_t beg = c > t0 ? (uint32_t)(c - t0) : 0u;
+      s_beg[idx] = beg;
+      s_off[idx] = rowoff[klo + idx] + (t0 + beg - c);
+      if (p1) s_u[idx] = flist[klo + idx];
+    }
+    if (threadIdx.x == 0) s_beg[cnt] = 0xFFFFFFFFu;
+    __syncthreads();
+    const uint32_t le = threadIdx.x * E;
+    if (le < len) {
+      // greatest idx < cnt with s_beg[idx] <= le (binsearch_maxle, Alg.3 line 2)
+      uint32_t lo = 0, hi = cnt - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (s_beg[mid] <= le) lo = mid; else hi = mid - 1;
+      }
+      uint32_t idx = lo;
+      uint32_t v[E], uq[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const uint32_t e = le + q;
+        if (e < len) {
+          while (s_beg[idx + 1] <= e) ++idx;                              // linear advance
+          v[q] = ld_stream_u32(row + s_off[idx] + (e - s_beg[idx]));      // Alg.3 line 4
+          uq[q] = idx;
+        } else {
+          v[q] = 0xFFFFFFFFu;
+        }
+      }
+      uint2 w[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) w[q] = (v[q] != 0xFFFFFFFFu) ? ld_cg_u2(vd + 2 * (v[q] >> 5)) : make_uint2(~0u, 0u);
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const uint32_t m = 1u << (v[q] & 31);
+        if (w[q].x & m) continue;  // visited (Alg.3 lines 5-6)
+        if (p1) {                  // parent claim: minimum global id (R1)
+          const uint32_t ug = col_base + s_u[uq[q]];
+          if (ug < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug);
+        }
+        if (!(w[q].y & m)) red_or(vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7 (skip if already set)
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int E>
 static cudaError_t launch_expand_t(const Geom& g, Rank& rk, cudaStream_t s) {
   constexpr int TILE = kExpandThreads * E;
@@ -290,8 +318,8 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, cudaStream_t s) {
     if (blocks_per_sm <= 0) blocks_per_sm = 1;
   }
   const int grid = num_sms() * blocks_per_sm;
-  k_expand<E><<<grid, kExpandThreads, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.info,
-                                                  rk.visited, rk.pred, rk.disc, (uint32_t)(rk.j * g.ncols()));
+  k_expand<E><<<grid, kExpandThreads, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.info, rk.vd,
+                                                  rk.pmin, (uint32_t)((uint64_t)rk.j * g.ncols()));
   return cudaGetLastError();
 }
 
@@ -306,27 +334,150 @@ cudaError_t launch_expand(const Geom& g, Rank& rk, int E, cudaStream_t s) {
   }
 }
 
+// ------------------------------------------------------------------ K4: parent claim
+// For every row discovered in this level (discovered words exclude visited rows):
+//   P1 levels: pred[r] = pmin[r] (the atomicMin result of the expansion); pmin[r] = UINT32_MAX.
+//   P2 levels: pred[r] = the minimum frontier column adjacent to r on this rank = the first
+//     entry of its ascending CSR row set in the frontier bitmap being expanded (all_front).
+//     Lanes scan their own rows 4 entries at a time for up to kShortScan entries; rows without a
+//     hit by then are finished by the whole warp, 32 entries per step (ballot -> first lane).
+// A warp takes 32 consecutive words and queues their rows in shared memory.  With C > 1 the
+// discovered words are also packed contiguously as the fold message.
+constexpr int kParentThreads = 256;
+constexpr int kShortScan = 32;
+
+__global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __restrict__ vd, uint64_t nwords,
+                                                            const ull* __restrict__ csr_ptr,
+                                                            const uint32_t* __restrict__ csr_col,
+                                                            const uint32_t* __restrict__ front, uint32_t* pred,
+                                                            uint32_t* pmin, uint32_t* sendbuf, uint32_t col_base,
+                                                            const LevelInfo* __restrict__ info) {
+  __shared__ uint32_t queue[kParentThreads / 32][1024];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool p1 = info->mode == 1;
+  const uint64_t nchunks = (nwords + 31) / 32;
+  for (uint64_t ch = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid; ch < nchunks;
+       ch += (uint64_t)gridDim.x * (kParentThreads / 32)) {
+    const uint64_t w = ch * 32 + lane;
+    const uint32_t d = (w < nwords) ? vd[2 * w + 1] : 0u;
+    if (sendbuf && w < nwords) sendbuf[w] = d;
+    if (!__any_sync(0xFFFFFFFFu, d != 0)) continue;
+    if (p1) {
+      uint32_t b = d;
+      while (b) {
+        const int bit = __ffs(b) - 1;
+        b &= b - 1;
+        const uint64_t r = w * 32 + bit;
+        pred[r] = pmin[r];
+        pmin[r] = 0xFFFFFFFFu;
+      }
+      continue;
+    }
+    // exclusive prefix of popcounts across lanes -> queue positions
+    const unsigned c = __popc(d);
+    unsigned inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const unsigned total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    unsigned pos = inc - c;
+    uint32_t b = d;
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      queue[wid][pos++] = (uint32_t)(w * 32 + bit);
+    }
+    __syncwarp();
+    unsigned nlong = 0;  // lane-local count of deferred rows (written at slots lane, lane+32, ...)
+    for (unsigned q = lane; q < total; q += 32) {
+      const uint32_t r = queue[wid][q];
+      const ull beg = csr_ptr[r], end = csr_ptr[r + 1];
+      const ull stop = min(end, beg + kShortScan);
+      uint32_t best = 0xFFFFFFFFu;
+      ull p = beg;
+      for (; p < stop && best == 0xFFFFFFFFu; p += 4) {
+        uint32_t u[4];
+        bool f[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = (p + k < stop) ? __ldg(csr_col + p + k) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          f[k] = (u[k] != 0xFFFFFFFFu) && ((__ldg(front + (u[k] >> 5)) >> (u[k] & 31)) & 1u);
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+          if (f[k]) best = u[k];
+      }
+      if (best != 0xFFFFFFFFu) {
+        pred[r] = col_base + best;
+      } else {  // defer to the whole warp; slot lane+32*nlong <= q was already consumed
+        queue[wid][lane + 32 * nlong] = r;
+        ++nlong;
+      }
+    }
+    __syncwarp();
+    // cooperative scan of the deferred rows: lane l's k-th row sits at slot l + 32k
+    unsigned maxlong = nlong;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) maxlong = max(maxlong, __shfl_xor_sync(0xFFFFFFFFu, maxlong, o));
+    for (unsigned k = 0; k < maxlong; ++k) {
+      unsigned has = __ballot_sync(0xFFFFFFFFu, k < nlong);
+      while (has) {
+        const int src = __ffs(has) - 1;
+        has &= has - 1;
+        const uint32_t r = queue[wid][src + 32 * k];
+        const ull end = csr_ptr[r + 1];
+        uint32_t best = 0xFFFFFFFFu;
+        for (ull p = csr_ptr[r] + kShortScan; p < end; p += 32) {
+          const uint32_t u = (p + lane < end) ? __ldg(csr_col + p + lane) : 0xFFFFFFFFu;
+          const bool f = (u != 0xFFFFFFFFu) && ((__ldg(front + (u >> 5)) >> (u & 31)) & 1u);
+          const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
+          if (m) {
+            best = __shfl_sync(0xFFFFFFFFu, u, __ffs(m) - 1);
+            break;
+          }
+        }
+        if (lane == 0) pred[r] = col_base + best;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
+  const uint64_t nwords = g.nrows() / 32;
+  const uint64_t nchunks = (nwords + 31) / 32;
+  uint64_t grid = (nchunks + kParentThreads / 32 - 1) / (kParentThreads / 32);
+  const uint64_t cap = (uint64_t)num_sms() * 4;
+  if (grid > cap) grid = cap;
+  k_parent<<<(unsigned)grid, kParentThreads, 0, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
+                                                     rk.pmin, g.C > 1 ? rk.sendbuf : nullptr,
+                                                     (uint32_t)((uint64_t)rk.j * g.ncols()), rk.info);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K2: frontier update
 // Thread per (segment m, word w) of the local rows.  Owned segment m == j: new vertices are the
 // rows received from any column (own discoveries included) that are not yet visited; the
 // lowest sending column is recorded as the parent's column (winner).  Other segments: mark the
 // rows this rank discovered as visited so they are sent at most once.
-__global__ void __launch_bounds__(256) k_update(uint32_t* visited, uint32_t* disc, const uint32_t* recv,
-                                                uint32_t* front_seg, int32_t* level, uint8_t* winner,
-                                                LevelInfo* info, uint64_t W, int C, int j, int lvl) {
+__global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* recv, uint32_t* front_seg,
+                                                int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
+                                                int j, int lvl) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t newbits = 0;
   if (gid < W * (uint64_t)C) {
     const int m = (int)(gid / W);
     const uint64_t w = gid - (uint64_t)m * W;
+    uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
     if (m != j) {
-      visited[gid] |= disc[gid];
-      disc[gid] = 0;
+      if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
     } else {
-      const uint32_t vis = visited[gid];
+      const uint32_t vis = p.x;
       uint32_t claimed = 0;
       for (int c = 0; c < C; ++c) {
-        const uint32_t x = ((c == j) ? disc[gid] : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
+        const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
         if (x && winner) {
           uint32_t b = x;
           while (b) {
@@ -338,8 +489,7 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* visited, uint32_t* dis
         claimed |= x;
       }
       newbits = claimed;
-      visited[gid] = vis | newbits;
-      disc[gid] = 0;
+      if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
       front_seg[w] = newbits;
       uint32_t b = newbits;
       while (b) {
@@ -349,7 +499,7 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* visited, uint32_t* dis
       }
     }
   }
-  unsigned int cnt = __popc(newbits);
+  unsigned cnt = __popc(newbits);
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&info->newv, (ull)cnt);
@@ -359,40 +509,42 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
   const uint64_t W = g.words_block();
   const uint64_t nthreads = W * (uint64_t)g.C;
   const unsigned grid = (unsigned)((nthreads + 255) / 256);
-  k_update<<<grid, 256, 0, s>>>(rk.visited, rk.disc, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
+  k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
                                 g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, lvl);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ outputs
-// parent for owned t: unreached -> -1; winner column == own column (always with C == 1) ->
-// pred of the own row segment; otherwise left for the resolution exchange.
-__global__ void k_finalize(const int32_t* level, const uint32_t* pred_own, const uint8_t* winner, int j,
-                           uint64_t block, int64_t* parent_out, int32_t* level_out) {
+// For owned t: unreached (visited bit clear) -> level -1, parent -1; reached with the winner
+// column == own column (always when C == 1) -> parent = pred of the own row segment; other
+// reached vertices are filled by the resolution exchange (k_resp_scatter).
+__global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const uint32_t* pred_own,
+                           const uint8_t* winner, int j, uint64_t block, int64_t* parent_out, int32_t* level_out) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= block) return;
-  const int32_t lv = level[t];
+  const bool reached = (vd_own[2 * (t >> 5)] >> (t & 31)) & 1u;
   if (parent_out) {
     int64_t p = -1;
-    if (lv >= 0 && (!winner || winner[t] == (uint8_t)j)) p = (int64_t)pred_own[t];
+    if (reached && (!winner || winner[t] == (uint8_t)j)) p = (int64_t)pred_own[t];
     parent_out[t] = p;
   }
-  if (level_out) level_out[t] = lv;
+  if (level_out) level_out[t] = reached ? level[t] : -1;
 }
 
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
   const unsigned grid = (unsigned)((g.block + 255) / 256);
-  k_finalize<<<grid, 256, 0, s>>>(rk.level, rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.j,
-                                  g.block, parent_out, level_out);
+  k_finalize<<<grid, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.level,
+                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.j, g.block,
+                                  parent_out, level_out);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ parent resolution (C > 1)
 // request bitmaps: req[c] has bit t for owned reached t whose winner column is c != j
-__global__ void k_req_build(const uint32_t* vis_own, const uint8_t* winner, uint32_t* req, uint64_t W, int C, int j) {
+__global__ void k_req_build(const uint32_t* vd_own, const uint8_t* winner, uint32_t* req, uint64_t W, int C, int j) {
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= W) return;
-  uint32_t b = vis_own[w];
+  uint32_t b = vd_own[2 * w];  // visited word
   while (b) {
     const int bit = __ffs(b) - 1;
     b &= b - 1;
@@ -404,8 +556,8 @@ __global__ void k_req_build(const uint32_t* vis_own, const uint8_t* winner, uint
 cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t W = g.words_block();
   cudaMemsetAsync(rk.req, 0, W * g.C * 4, s);
-  k_req_build<<<(unsigned)((W + 255) / 256), 256, 0, s>>>(rk.visited + (uint64_t)rk.j * W, rk.winner, rk.req, W, g.C,
-                                                           rk.j);
+  k_req_build<<<(unsigned)((W + 255) / 256), 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * W, rk.winner, rk.req, W,
+                                                           g.C, rk.j);
   return cudaGetLastError();
 }
 
@@ -480,18 +632,18 @@ cudaError_t launch_resp_scatter(const Geom& g, Rank& rk, int64_t* parent_out, cu
 }
 
 // ------------------------------------------------------------------ m_comp, degree
-__global__ void __launch_bounds__(256) k_mcomp(const int32_t* level, const uint32_t* tdeg, uint64_t block, ull* out) {
+__global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uint32_t* tdeg, uint64_t block, ull* out) {
   typedef cub::BlockReduce<ull, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   ull acc = 0;
   for (uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x; t < block; t += (uint64_t)gridDim.x * 256)
-    if (level[t] >= 0) acc += tdeg[t];
+    if ((vd_own[2 * (t >> 5)] >> (t & 31)) & 1u) acc += tdeg[t];
   ull tot = BR(tmp).Sum(acc);
   if (threadIdx.x == 0 && tot) atomicAdd(out, tot);
 }
 
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, ull* out, cudaStream_t s) {
-  k_mcomp<<<num_sms() * 4, 256, 0, s>>>(rk.level, rk.tdeg, g.block, out);
+  k_mcomp<<<num_sms() * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, g.block, out);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,9 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 // K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
 cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, cudaStream_t s);
 
+// K4: parent claim for the rows discovered in this level (+ pack of the fold message, C > 1).
+cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s);
+
 // K2: frontier update + pack; lvl is the level being assigned.
 cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s);
 
