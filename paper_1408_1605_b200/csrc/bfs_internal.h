@@ -26,6 +26,8 @@ struct LevelInfo {
   unsigned long long newv;   // vertices discovered by the update (this rank)
   unsigned long long mode;   // parent claim of this level: 1 = atomicMin in the expansion (P1),
                              // 2 = CSR scan of the discovered rows (P2); see k_scan_segs
+  unsigned long long nlong;  // long columns whose tile-table range is filled by k_tile_fill
+  unsigned long long pad[3];
 };
 
 // Geometry of the 2D partition (index maps SPEC.md S:109-148).
@@ -47,7 +49,12 @@ struct Rank {
   // with R = C = 1 the matrix is symmetric and these alias col/row.
   unsigned long long* csr_ptr = nullptr;  // [nrows+1]
   uint32_t* csr_col = nullptr;            // [nnz]
-  uint32_t* tdeg = nullptr;   // [block] input tuples whose source is the owned vertex (m_comp)
+  uint32_t* tdeg = nullptr;   // [block] input tuples whose source is the owned vertex (m_comp), ORIGINAL offsets
+  // hot-prefix relabeling maps (build_graph.cu): owned offsets original <-> relabeled, and the
+  // ORIGINAL global id of every relabeled local column (the value stored as a parent)
+  uint32_t* fwd_own = nullptr;  // [block]
+  uint32_t* inv_own = nullptr;  // [block]
+  uint32_t* inv_col = nullptr;  // [ncols]
   // per-search state
   // visited bitmap over ALL local rows interleaved word by word with the
   // rows discovered in the current level: vd[2w] = visited word w, vd[2w+1] = discovered word w,
@@ -63,7 +70,8 @@ struct Rank {
   uint32_t* flist = nullptr;     // [ncols] frontier columns with degree>0, ascending
   unsigned long long* rowoff = nullptr;  // [ncols] col[flist[k]]
   unsigned long long* cumul = nullptr;   // [ncols+1] exclusive scan of degrees
-  uint32_t* tile_k = nullptr;            // [nnz/256 + 2] first frontier index of every expansion tile
+  uint32_t* tile_k = nullptr;            // [nnz/32 + 2] first frontier index of every expansion tile
+  uint4* longlist = nullptr;             // [nnz/128 + 64] (first tile, #tiles, column index) of long columns
   uint32_t* seg_cnt = nullptr;           // [nseg] per-segment frontier count (degree > 0)
   unsigned long long* seg_sum = nullptr; // [nseg] per-segment degree sum
   uint32_t* seg_cnt_off = nullptr;       // exclusive scans of the above
@@ -94,6 +102,8 @@ struct Graph {
   bool broken = false;
   std::vector<Rank> ranks;  // local ranks (all R*C with loopback)
   std::vector<void*> allocs;  // graph-lifetime device allocations
+  uint64_t hot_h = 0;         // relabeled hot prefix per vertex block (vertices)
+  uint32_t* perm_fwd = nullptr;  // [npad] original -> relabeled global id
   LevelInfo* infos = nullptr; // [nlocal] device, one per local rank
   LevelInfo* h_infos = nullptr; // pinned mirror
   unsigned long long* dscratch = nullptr; // [16] device scratch for reductions

@@ -1,15 +1,24 @@
-// build_graph.cu -- graph construction: tuples -> 2D partition -> per-rank CSC (not timed).
+// build_graph.cu -- graph construction: tuples -> 2D partition -> per-rank CSC/CSR (not timed).
 //
 // PAPER.md P:300-303 ("the graph is partitioned as described in Section 2DPart")
 // (symmetrise), P:275-291 (local (N/R) x (N/C) matrix stored as CSC: `col` offsets + `row`
 // indices).  Each tuple (a, b), a != b, is inserted as edge a->b and b->a; edge u->v goes to
 // P_ij with i = (v/block) mod R, j = u/(N/C) as column
 // local_col(u) = u mod N/C and row local_row(v) = (v/block/R)*block + v mod block.
-// Duplicates collapse and self-loops are dropped; rows are ascending within a
-// column.  tdeg[v] counts every input tuple with source v (the m_comp numerator,
-// P:695-698), duplicates and self-loops included.
+// Duplicates collapse and self-loops are dropped.  tdeg[v] counts every input
+// tuple with source v (the m_comp numerator), duplicates and self-loops included.
+//
+// Internal relabeling (layout only): inside every vertex block the H vertices of
+// highest tuple degree are moved to offsets 0..H-1 (degree order), swapping places with the
+// vertices they displace; ownership (the block) never changes and all outputs are in the
+// original ids.  The expansion keeps the visited bits of these hot prefixes in shared memory.
+// To keep the minimum-id parent rule in original ids, CSC rows are ordered by ORIGINAL row id
+// and CSR rows by ORIGINAL column id (the stored indices are the relabeled ones).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <vector>
 
 #include "engine.h"
 
@@ -25,8 +34,9 @@ struct PartMap {
     const int j = (int)(u / ncols);
     return j * R + i;
   }
-  __device__ __forceinline__ ull key(uint64_t u, uint64_t v) const {
-    const uint64_t lc = u % ncols;
+  // CSC sort key: relabeled local column, then ORIGINAL local row
+  __device__ __forceinline__ ull key(uint64_t u, uint64_t v, const uint32_t* fwd) const {
+    const uint64_t lc = (uint64_t)fwd[u] % ncols;
     const uint64_t lr = (v / block / (uint64_t)R) * block + v % block;
     return ((ull)lc << rbits) | (ull)lr;
   }
@@ -36,10 +46,11 @@ constexpr int kBuildThreads = 256;
 constexpr int kBuildPer = 8;  // tuples per thread per CTA chunk
 constexpr int kMaxP = 64;
 
-// count directed entries per destination rank; validate ids; tuple-source histogram
+// count directed entries per destination rank; validate ids; tuple-source histogram (tdeg)
+// and endpoint histogram (sdeg, non-self-loop, for the hot-prefix relabeling)
 __global__ void __launch_bounds__(kBuildThreads) k_count(const uint64_t* src, const uint64_t* dst, uint64_t m,
                                                          PartMap pm, int P, ull* counts, uint32_t* tdeg_all,
-                                                         int* err) {
+                                                         uint32_t* sdeg_all, int* err) {
   __shared__ unsigned int sc[kMaxP];
   for (int q = threadIdx.x; q < P; q += blockDim.x) sc[q] = 0;
   __syncthreads();
@@ -52,8 +63,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_count(const uint64_t* src, co
       atomicOr(err, 1);
       continue;
     }
-    if (tdeg_all) atomicAdd(tdeg_all + a, 1u);
+    atomicAdd(tdeg_all + a, 1u);
     if (a == b) continue;
+    atomicAdd(sdeg_all + a, 1u);
+    atomicAdd(sdeg_all + b, 1u);
     atomicAdd(&sc[pm.dest(a, b)], 1u);
     atomicAdd(&sc[pm.dest(b, a)], 1u);
   }
@@ -64,7 +77,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_count(const uint64_t* src, co
 
 // scatter keys into per-destination buckets; cursors[r] starts at the bucket offset
 __global__ void __launch_bounds__(kBuildThreads) k_scatter(const uint64_t* src, const uint64_t* dst, uint64_t m,
-                                                           PartMap pm, int P, ull* cursors, ull* keys) {
+                                                           PartMap pm, int P, ull* cursors, ull* keys,
+                                                           const uint32_t* fwd) {
   __shared__ unsigned int sc[kMaxP];
   __shared__ ull sbase[kMaxP];
   for (int q = threadIdx.x; q < P; q += blockDim.x) sc[q] = 0;
@@ -90,37 +104,84 @@ __global__ void __launch_bounds__(kBuildThreads) k_scatter(const uint64_t* src, 
   __syncthreads();
   for (int q = 0; q < kBuildPer; ++q) {
     if (d1[q] < 0) continue;
-    keys[sbase[d1[q]] + pos1[q]] = pm.key(a[q], b[q]);
-    keys[sbase[d2[q]] + pos2[q]] = pm.key(b[q], a[q]);
+    keys[sbase[d1[q]] + pos1[q]] = pm.key(a[q], b[q], fwd);
+    keys[sbase[d2[q]] + pos2[q]] = pm.key(b[q], a[q], fwd);
   }
 }
 
-__global__ void k_keys_to_rows(const ull* keys, uint64_t n, ull rmask, uint32_t* row) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
-    row[t] = (uint32_t)(keys[t] & rmask);
+// ---- relabeling helpers
+__global__ void k_degree_keys(const uint32_t* sdeg, uint64_t npad, uint64_t block, ull* keys, uint32_t* vals) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < npad; v += (uint64_t)gridDim.x * blockDim.x) {
+    keys[v] = ((ull)(v / block) << 32) | (ull)(0xFFFFFFFFu - sdeg[v]);  // block, then degree descending
+    vals[v] = (uint32_t)v;
+  }
 }
 
-// CSC key (col << rbits | row) -> CSR key (row << cbits | col)
-__global__ void k_swap_keys(ull* keys, uint64_t n, int rbits, int cbits) {
+__global__ void k_iota2(uint32_t* a, uint32_t* b, uint64_t n) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+    a[v] = b[v] = (uint32_t)v;
+}
+
+__global__ void k_apply_moves(const uint32_t* moves, uint64_t nmoves, uint32_t* fwd, uint32_t* inv) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nmoves; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = moves[2 * t], n = moves[2 * t + 1];
+    fwd[o] = n;
+    inv[n] = o;
+  }
+}
+
+// ---- CSC / CSR assembly
+// row[t] = relabeled local row of the ORIGINAL local row in the key's low bits
+__global__ void k_keys_to_rows(const ull* keys, uint64_t n, int rbits, uint64_t block, int R, int i,
+                               const uint32_t* fwd, uint32_t* row) {
+  const ull rmask = (1ull << rbits) - 1;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lr = keys[t] & rmask;
+    const uint64_t m = lr / block;
+    const uint64_t vb = (m * R + i) * block;  // first global id of the row's vertex block
+    row[t] = (uint32_t)(m * block + (fwd[vb + lr % block] - vb));
+  }
+}
+
+// CSC key (col' << rbits | orig row) -> CSR key (row' << cbits | orig col)
+__global__ void k_csr_keys(ull* keys, uint64_t n, int rbits, int cbits, uint64_t block, int R, int i, uint64_t cbase,
+                           const uint32_t* fwd, const uint32_t* inv) {
   const ull rmask = (1ull << rbits) - 1;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
     const ull k = keys[t];
-    keys[t] = ((k & rmask) << cbits) | (k >> rbits);
+    const uint64_t lr = k & rmask, lc = k >> rbits;
+    const uint64_t m = lr / block;
+    const uint64_t vb = (m * R + i) * block;
+    const uint64_t lr2 = m * block + (fwd[vb + lr % block] - vb);
+    const uint64_t lc_orig = inv[cbase + lc] - cbase;
+    keys[t] = ((ull)lr2 << cbits) | (ull)lc_orig;
   }
 }
 
-// col[c] = first position with key >= c << rbits (lower bound), c in [0, ncols]
-__global__ void k_col_offsets(const ull* keys, uint64_t n, int rbits, uint64_t ncols, ull* col) {
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= ncols;
-       c += (uint64_t)gridDim.x * blockDim.x) {
-    const ull target = (ull)c << rbits;
+// csr_col[t] = relabeled local column of the ORIGINAL local column in the key's low bits
+__global__ void k_keys_to_cols(const ull* keys, uint64_t n, int cbits, uint64_t cbase, const uint32_t* fwd,
+                               uint32_t* out) {
+  const ull cmask = (1ull << cbits) - 1;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    out[t] = (uint32_t)(fwd[cbase + (keys[t] & cmask)] - cbase);
+}
+
+// off[c] = first position with key >= c << shift (lower bound), c in [0, nc]
+__global__ void k_offsets(const ull* keys, uint64_t n, int shift, uint64_t nc, ull* off) {
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += (uint64_t)gridDim.x * blockDim.x) {
+    const ull target = (ull)c << shift;
     uint64_t lo = 0, hi = n;
     while (lo < hi) {
       const uint64_t mid = (lo + hi) >> 1;
       if (keys[mid] < target) lo = mid + 1; else hi = mid;
     }
-    col[c] = lo;
+    off[c] = lo;
   }
+}
+
+__global__ void k_slice(const uint32_t* src, uint64_t base, uint64_t n, uint32_t sub, uint32_t* dst) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    dst[t] = src[base + t] - sub;
 }
 
 static int bits_for(uint64_t n) {  // bits to represent values < n
@@ -129,11 +190,76 @@ static int bits_for(uint64_t n) {  // bits to represent values < n
   return b;
 }
 
-// Sorted/deduplicated CSC for one rank from its bucket of keys (consumed: used as scratch).
-static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits) {
+// Hot-prefix permutation: perm_fwd (original -> relabeled global id) and perm_inv on device.
+static int compute_relabel(Graph& G, const uint32_t* sdeg, uint32_t* fwd, uint32_t* inv) {
   cudaStream_t s = G.stream;
   const Geom& g = G.g;
-  const int kbits = rbits + bits_for(g.ncols());
+  const uint64_t P = (uint64_t)g.R * g.C;
+  const uint64_t H = G.hot_h;
+  Scratch sc;
+  k_iota2<<<4096, 256, 0, s>>>(fwd, inv, g.npad);
+  CKR(cudaGetLastError());
+  if (H == 0) return BFS_OK;
+  ull *keys = nullptr, *keys2 = nullptr;
+  uint32_t *vals = nullptr, *vals2 = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const int kb = 32 + bits_for(P);
+  CKR(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (uint64_t)g.npad, 0, kb, s));
+  CKR(sc.alloc(&keys, g.npad * 8));
+  CKR(sc.alloc(&keys2, g.npad * 8));
+  CKR(sc.alloc(&vals, g.npad * 4));
+  CKR(sc.alloc(&vals2, g.npad * 4));
+  CKR(sc.alloc(&tmp, tmp_bytes));
+  k_degree_keys<<<4096, 256, 0, s>>>(sdeg, g.npad, g.block, keys, vals);
+  CKR(cudaGetLastError());
+  CKR(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (uint64_t)g.npad, 0, kb, s));
+  std::vector<uint32_t> hot(P * H);
+  for (uint64_t b = 0; b < P; ++b)
+    CKR(cudaMemcpyAsync(hot.data() + b * H, vals2 + b * g.block, H * 4, cudaMemcpyDeviceToHost, s));
+  CKR(cudaStreamSynchronize(s));
+  // moves: hot vertex t_q -> offset q; displaced occupant of a low offset q -> a vacated offset
+  std::vector<uint32_t> moves;
+  moves.reserve(P * H * 4);
+  std::vector<char> low_hot(H);
+  for (uint64_t b = 0; b < P; ++b) {
+    const uint64_t vb = b * g.block;
+    std::fill(low_hot.begin(), low_hot.end(), 0);
+    std::vector<uint64_t> vacated;
+    for (uint64_t q = 0; q < H; ++q) {
+      const uint64_t t = hot[b * H + q] - vb;
+      if (t < H) low_hot[t] = 1; else vacated.push_back(t);
+      if (t != q) {
+        moves.push_back((uint32_t)(vb + t));
+        moves.push_back((uint32_t)(vb + q));
+      }
+    }
+    size_t k = 0;
+    for (uint64_t q = 0; q < H; ++q)
+      if (!low_hot[q]) {
+        moves.push_back((uint32_t)(vb + q));
+        moves.push_back((uint32_t)(vb + vacated[k++]));
+      }
+  }
+  const uint64_t nm = moves.size() / 2;
+  if (nm) {
+    uint32_t* dm = nullptr;
+    CKR(sc.alloc(&dm, moves.size() * 4));
+    CKR(cudaMemcpyAsync(dm, moves.data(), moves.size() * 4, cudaMemcpyHostToDevice, s));
+    k_apply_moves<<<1024, 256, 0, s>>>(dm, nm, fwd, inv);
+    CKR(cudaGetLastError());
+  }
+  CKR(cudaStreamSynchronize(s));
+  return BFS_OK;
+}
+
+// Sorted/deduplicated CSC (and, for 2D, CSR) of one rank from its bucket of keys (consumed).
+static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, const uint32_t* fwd,
+                         const uint32_t* inv) {
+  cudaStream_t s = G.stream;
+  const Geom& g = G.g;
+  const int cbits = bits_for(g.ncols());
+  const int kbits = rbits + cbits;
   Scratch sc;
   ull* sorted = nullptr;
   void* tmp = nullptr;
@@ -155,6 +281,7 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits) {
     sc.release(sorted);
     sc.release(tmp);
     sc.release(nsel);
+    sorted = nullptr;
     rk.nnz = h_nsel;
   } else {
     rk.nnz = 0;
@@ -164,44 +291,62 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits) {
   rc = G_alloc(G, (void**)&rk.col, (g.ncols() + 1) * sizeof(ull));
   if (rc) return rc;
   if (rk.nnz) {
-    k_keys_to_rows<<<4096, 256, 0, s>>>(keys, rk.nnz, (rbits >= 64) ? ~0ull : ((1ull << rbits) - 1), rk.row);
+    k_keys_to_rows<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, g.block, g.R, rk.i, fwd, rk.row);
     CKR(cudaGetLastError());
   }
   const uint64_t nc = g.ncols() + 1;
-  k_col_offsets<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(keys, rk.nnz, rbits, g.ncols(), rk.col);
+  k_offsets<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(keys, rk.nnz, rbits, g.ncols(), rk.col);
   CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
-  // CSR of the same local matrix for the parent pass (rows scanned in ascending column order).
-  // With a 1x1 grid the matrix is the symmetric adjacency, so the CSC already is its CSR.
+  // CSR of the same local matrix for the parent pass (rows scanned in ascending ORIGINAL
+  // column order).  With a 1x1 grid the matrix is the symmetric adjacency and its CSC (rows in
+  // ascending original order) already is that CSR.
   if (g.R * g.C == 1) {
     rk.csr_ptr = rk.col;
     rk.csr_col = rk.row;
     return BFS_OK;
   }
-  const int cbits = bits_for(g.ncols());
+  const uint64_t cbase = (uint64_t)rk.j * g.ncols();
   rc = G_alloc(G, (void**)&rk.csr_col, (rk.nnz ? rk.nnz : 1) * sizeof(uint32_t));
   if (rc) return rc;
   rc = G_alloc(G, (void**)&rk.csr_ptr, (g.nrows() + 1) * sizeof(ull));
   if (rc) return rc;
   if (rk.nnz) {
-    k_swap_keys<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, cbits);
+    k_csr_keys<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, cbits, g.block, g.R, rk.i, cbase, fwd, inv);
     CKR(cudaGetLastError());
     tmp_bytes = 0;
     CKR(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys, (uint64_t)rk.nnz, 0, rbits + cbits, s));
     CKR(sc.alloc(&sorted, rk.nnz * sizeof(ull)));
     CKR(sc.alloc(&tmp, tmp_bytes));
     CKR(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (uint64_t)rk.nnz, 0, rbits + cbits, s));
-    k_keys_to_rows<<<4096, 256, 0, s>>>(sorted, rk.nnz, (1ull << cbits) - 1, rk.csr_col);
+    k_keys_to_cols<<<4096, 256, 0, s>>>(sorted, rk.nnz, cbits, cbase, fwd, rk.csr_col);
     CKR(cudaGetLastError());
   }
   const uint64_t nr = g.nrows() + 1;
-  k_col_offsets<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(sorted, rk.nnz, cbits, g.nrows(), rk.csr_ptr);
+  k_offsets<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(sorted, rk.nnz, cbits, g.nrows(), rk.csr_ptr);
   CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
   return BFS_OK;
 }
 
-// Build every local rank's CSC and tdeg.  src/dst: host or device arrays of m tuples.
+// per-rank slices of the permutation: fwd_own / inv_own (local offsets of the owned block) and
+// inv_col (relabeled local column -> ORIGINAL global id, the value stored as parent)
+static int rank_maps(Graph& G, Rank& rk, const uint32_t* fwd, const uint32_t* inv) {
+  cudaStream_t s = G.stream;
+  const Geom& g = G.g;
+  int rc;
+  if ((rc = G_alloc(G, (void**)&rk.fwd_own, g.block * 4))) return rc;
+  if ((rc = G_alloc(G, (void**)&rk.inv_own, g.block * 4))) return rc;
+  if ((rc = G_alloc(G, (void**)&rk.inv_col, g.ncols() * 4))) return rc;
+  const uint64_t vb = (uint64_t)rk.r * g.block;
+  k_slice<<<1024, 256, 0, s>>>(fwd, vb, g.block, (uint32_t)vb, rk.fwd_own);
+  k_slice<<<1024, 256, 0, s>>>(inv, vb, g.block, (uint32_t)vb, rk.inv_own);
+  k_slice<<<1024, 256, 0, s>>>(inv, (uint64_t)rk.j * g.ncols(), g.ncols(), 0u, rk.inv_col);
+  CKR(cudaGetLastError());
+  return BFS_OK;
+}
+
+// Build every local rank's CSC/CSR, maps and tdeg.  src/dst: host or device arrays of m tuples.
 int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) {
   cudaStream_t s = G.stream;
   const Geom& g = G.g;
@@ -211,15 +356,17 @@ int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) 
   const bool src_dev = is_device_ptr(src), dst_dev = is_device_ptr(dst);
   if (src_dev != dst_dev) return set_err(BFS_EINVAL, "src and dst must both be host or both device pointers");
 
-  // ---- tuple-source histogram (whole vertex range) and per-destination counts
+  // ---- histograms and per-destination counts
   Scratch sc;
-  uint32_t* tdeg_all = nullptr;
+  uint32_t *tdeg_all = nullptr, *sdeg_all = nullptr;
   ull* counts = nullptr;
   int* err = nullptr;
   CKR(sc.alloc(&tdeg_all, g.npad * sizeof(uint32_t)));
+  CKR(sc.alloc(&sdeg_all, g.npad * sizeof(uint32_t)));
   CKR(sc.alloc(&counts, 2 * kMaxP * sizeof(ull)));
   CKR(sc.alloc(&err, sizeof(int)));
   CKR(cudaMemsetAsync(tdeg_all, 0, g.npad * sizeof(uint32_t), s));
+  CKR(cudaMemsetAsync(sdeg_all, 0, g.npad * sizeof(uint32_t), s));
   CKR(cudaMemsetAsync(counts, 0, 2 * kMaxP * sizeof(ull), s));
   CKR(cudaMemsetAsync(err, 0, sizeof(int), s));
   const uint64_t chunk = src_dev ? (m ? m : 1) : (1ull << 26);
@@ -248,7 +395,7 @@ int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) 
     return BFS_OK;
   };
   int rc = for_chunks([&](const uint64_t* ps, const uint64_t* pd, uint64_t len, unsigned grid) {
-    k_count<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, counts, tdeg_all, err);
+    k_count<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, counts, tdeg_all, sdeg_all, err);
   });
   if (rc) return rc;
   ull h_counts[kMaxP];
@@ -263,6 +410,19 @@ int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) 
     h_err = any_err;
   }
   if (h_err) return set_err(BFS_ERANGE, "an edge endpoint is >= nverts");
+  if (G.world_size > 1) {
+    rc = comm_allreduce_u32_sum(G, sdeg_all, g.npad);
+    if (rc) return rc;
+  }
+
+  // ---- hot-prefix relabeling (perm_fwd kept for root / degree lookups)
+  uint32_t* inv = nullptr;
+  rc = G_alloc(G, (void**)&G.perm_fwd, g.npad * 4);
+  if (rc) return rc;
+  CKR(sc.alloc(&inv, g.npad * 4));
+  rc = compute_relabel(G, sdeg_all, G.perm_fwd, inv);
+  if (rc) return rc;
+  sc.release(sdeg_all);
 
   // ---- bucket keys by destination rank
   ull offs[kMaxP + 1];
@@ -273,21 +433,27 @@ int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) 
   ull* cursors = counts + kMaxP;
   CKR(cudaMemcpyAsync(cursors, offs, P * sizeof(ull), cudaMemcpyHostToDevice, s));
   rc = for_chunks([&](const uint64_t* ps, const uint64_t* pd, uint64_t len, unsigned grid) {
-    k_scatter<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, cursors, keys);
+    k_scatter<<<grid, kBuildThreads, 0, s>>>(ps, pd, len, pm, P, cursors, keys, G.perm_fwd);
   });
   if (rc) return rc;
   CKR(cudaStreamSynchronize(s));
-  if (stage_s) { sc.release(stage_s); sc.release(stage_d); stage_s = stage_d = nullptr; }
+  if (stage_s) {
+    sc.release(stage_s);
+    sc.release(stage_d);
+    stage_s = stage_d = nullptr;
+  }
 
   if (G.world_size == 1) {
     // loopback (or 1x1): every bucket is local
     for (Rank& rk : G.ranks) {
-      rc = csc_from_keys(G, rk, keys + offs[rk.r], h_counts[rk.r], pm.rbits);
+      rc = csc_from_keys(G, rk, keys + offs[rk.r], h_counts[rk.r], pm.rbits, G.perm_fwd, inv);
       if (rc) return rc;
       rc = G_alloc(G, (void**)&rk.tdeg, g.block * sizeof(uint32_t));
       if (rc) return rc;
       CKR(cudaMemcpyAsync(rk.tdeg, tdeg_all + (uint64_t)rk.r * g.block, g.block * sizeof(uint32_t),
                           cudaMemcpyDeviceToDevice, s));
+      rc = rank_maps(G, rk, G.perm_fwd, inv);
+      if (rc) return rc;
     }
     CKR(cudaStreamSynchronize(s));
     sc.release(keys);
@@ -310,12 +476,14 @@ int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m) 
     if (rc) return rc;
     CKR(cudaStreamSynchronize(s));
     sc.release(keys);
-    rc = csc_from_keys(G, rk, rkeys, roffs[P], pm.rbits);
+    rc = csc_from_keys(G, rk, rkeys, roffs[P], pm.rbits, G.perm_fwd, inv);
     sc.release(rkeys);
     if (rc) return rc;
     rc = G_alloc(G, (void**)&rk.tdeg, g.block * sizeof(uint32_t));
     if (rc) return rc;
     rc = comm_reduce_scatter_u32(G, tdeg_all, rk.tdeg, g.block);
+    if (rc) return rc;
+    rc = rank_maps(G, rk, G.perm_fwd, inv);
     if (rc) return rc;
     CKR(cudaStreamSynchronize(s));
   }

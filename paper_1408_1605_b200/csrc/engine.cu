@@ -110,6 +110,11 @@ int comm_alltoallv_u64(Graph& G, const ull* send, const ull* soff, const ull* sc
   return BFS_OK;
 }
 
+int comm_allreduce_u32_sum(Graph& G, uint32_t* buf, uint64_t n) {
+  NKR(ncclAllReduce(buf, buf, n, ncclUint32, ncclSum, G.world, G.stream));
+  return BFS_OK;
+}
+
 int comm_reduce_scatter_u32(Graph& G, const uint32_t* full, uint32_t* mine, uint64_t block) {
   NKR(ncclReduceScatter(full, mine, block, ncclUint32, ncclSum, G.world, G.stream));
   return BFS_OK;
@@ -183,7 +188,8 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.flist, g.ncols() * 4);
   AL(rk.rowoff, g.ncols() * 8);
   AL(rk.cumul, (g.ncols() + 1) * 8);
-  AL(rk.tile_k, (rk.nnz / 256 + 2) * 4);
+  AL(rk.tile_k, (rk.nnz / 32 + 2) * 4);  // expansion tiles have >= 32 edges
+  AL(rk.longlist, (rk.nnz / 128 + 64) * 16);  // a long column spans > 8 tiles of >= 32 edges
   AL(rk.seg_cnt, nseg * 4);
   AL(rk.seg_sum, nseg * 8);
   AL(rk.seg_cnt_off, nseg * 4);
@@ -280,6 +286,7 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   G.g.R = R;
   G.g.C = C;
   G.g.block = G.g.npad / P;
+  G.hot_h = G.g.block < (1ull << 20) ? G.g.block : (1ull << 20);
   G.ntuples = nedges;
   CKR(cudaMallocHost(&G.h_scratch, 16 * sizeof(ull)));
   {
@@ -407,7 +414,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   const Geom& g = G.g;
   cudaStream_t s = G.stream;
   const int E = G.opts.edges_per_thread;
-  const uint32_t tile_edges = (uint32_t)(kExpandThreads * E);
+  const uint32_t tile_edges = expand_tile_edges(E);
   const uint64_t W = g.words_block();
   const uint64_t owner = root / g.block;
   bool owner_local = false;
@@ -427,7 +434,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     if ((rc = ev_rec(G, nlev, 1))) return rc;
     for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
     if ((rc = ev_rec(G, nlev, 2))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, s));
+    for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, s));
     for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
     if ((rc = ev_rec(G, nlev, 3))) return rc;
     if ((rc = fold_exchange(G))) return rc;
@@ -482,11 +489,11 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
     stats->bytes_exchanged = bytes;
     stats->reached = 0;
-    // own kernels: seed (owner only) + per level and local rank scan(3) + expand + parent +
+    // own kernels: seed (owner only) + per level and local rank scan(4) + expand + parent +
     // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals,
     // resp_pack, resp_scatter.
     const uint64_t nl = G.ranks.size();
-    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (6ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
+    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
   }
   return BFS_OK;
 }
@@ -596,10 +603,10 @@ int bfs_degree(bfs_graph* gp, uint64_t v, uint64_t* degree) {
   ENTER(gp);
   if (!degree) return set_err(BFS_EINVAL, "null output");
   if (v >= G.g.nverts) return set_err(BFS_ERANGE, "vertex %llu >= nverts", (ull)v);
-  const uint64_t jv = v / G.g.ncols(), u = v % G.g.ncols();
+  const uint64_t jv = v / G.g.ncols();  // relabeling stays inside vertex blocks, so columns too
   CKR(cudaMemsetAsync(G.dscratch, 0, sizeof(ull), G.stream));
   for (Rank& rk : G.ranks)
-    if ((uint64_t)rk.j == jv) CKR(launch_degree(rk, u, G.dscratch, G.stream));
+    if ((uint64_t)rk.j == jv) CKR(launch_degree(G.g, rk, G.perm_fwd, v, G.dscratch, G.stream));
   if (G.world_size > 1) NKR(ncclAllReduce(G.dscratch, G.dscratch, 1, ncclUint64, ncclSum, G.world, G.stream));
   CKR(cudaMemcpyAsync(G.h_scratch, G.dscratch, sizeof(ull), cudaMemcpyDeviceToHost, G.stream));
   CKR(cudaStreamSynchronize(G.stream));

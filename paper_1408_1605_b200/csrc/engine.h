@@ -55,6 +55,7 @@ int comm_exchange_counts(Graph& G, const unsigned long long* d_send_counts, unsi
 int comm_alltoallv_u64(Graph& G, const unsigned long long* send, const unsigned long long* soff,
                        const unsigned long long* scnt, unsigned long long* recv, const unsigned long long* roff,
                        const unsigned long long* rcnt);
+int comm_allreduce_u32_sum(Graph& G, uint32_t* buf, uint64_t n);
 int comm_reduce_scatter_u32(Graph& G, const uint32_t* full, uint32_t* mine, uint64_t block);
 
 int build_graph(Graph& G, const uint64_t* src, const uint64_t* dst, uint64_t m);

@@ -62,7 +62,9 @@ static int num_sms() {
 
 // ------------------------------------------------------------------ init (Alg.2 lines 1-10)
 __global__ void k_seed_root(uint32_t* vd, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
-                            uint64_t t, uint64_t row_local, uint64_t col_local, uint32_t root, int j) {
+                            const uint32_t* fwd_own, uint64_t t0, uint64_t block, int i, uint32_t root, int j) {
+  const uint64_t t = fwd_own[t0];  // relabeled offset of the root in its block
+  const uint64_t row_local = (uint64_t)j * block + t, col_local = (uint64_t)i * block + t;
   vd[2 * (row_local >> 5)] |= 1u << (row_local & 31);   // bmap[LOCAL_ROW(r)] <- 1
   all_front[col_local >> 5] |= 1u << (col_local & 31);  // front[0] <- LOCAL_COL(r)
   level[t] = 0;                                          // level[LOCAL_ROW(r)] <- 0
@@ -78,8 +80,8 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
   cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
   if (owner) {
     const uint64_t t = root - (uint64_t)rk.r * g.block;
-    k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, t, (uint64_t)rk.j * g.block + t,
-                                (uint64_t)rk.i * g.block + t, (uint32_t)root, rk.j);
+    k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
+                                (uint32_t)root, rk.j);
   }
   return cudaGetLastError();
 }
@@ -160,9 +162,10 @@ __global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const uint32_
     info->newv = 0;
     // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
     // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-    // the scan (P2) is used when that is <= 32; otherwise (small frontiers, e.g. the first
+    // the scan (P2) is used when that is <= 4; otherwise (small frontiers, e.g. the first
     // levels) the expansion does compare-then-atomicMin per candidate edge (P1).
-    info->mode = (carry.s * 32ull >= nnz) ? 2ull : 1ull;
+    info->mode = (carry.s * 4ull >= nnz) ? 2ull : 1ull;
+    info->nlong = 0;
     cumul[carry.c] = carry.s;
   }
 }
@@ -174,7 +177,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
                                                              uint64_t nseg, const ull* __restrict__ col,
                                                              const uint32_t* cnt_off, const ull* sum_off,
                                                              uint32_t* flist, ull* rowoff, ull* cumul,
-                                                             uint32_t* tile_k, uint32_t tile_edges) {
+                                                             uint32_t* tile_k, uint32_t tile_edges, uint4* longlist,
+                                                             LevelInfo* info) {
   const int lane = threadIdx.x & 31;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
   if (seg >= nseg) return;
@@ -209,11 +213,27 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         flist[pos] = (uint32_t)u;
         rowoff[pos] = c0;
         cumul[pos] = eb;
-        for (ull t = (eb + tile_edges - 1) / tile_edges; t * tile_edges < eb + d; ++t) tile_k[t] = (uint32_t)pos;
+        const ull tf = (eb + tile_edges - 1) / tile_edges, tl = (eb + d + tile_edges - 1) / tile_edges;
+        if (tl - tf <= 8) {
+          for (ull t = tf; t < tl; ++t) tile_k[t] = (uint32_t)pos;
+        } else {  // long column: the tile-table range is filled by k_tile_fill
+          const ull slot = atomicAdd(&info->nlong, 1ull);
+          longlist[slot] = make_uint4((uint32_t)tf, (uint32_t)(tl - tf), (uint32_t)pos, 0u);
+        }
       }
       k += __popc(mask);
       e += __shfl_sync(0xFFFFFFFFu, inc, 31);
     }
+  }
+}
+
+// tile-table ranges of long columns: one warp per range
+__global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint32_t* tile_k) {
+  const int lane = threadIdx.x & 31;
+  const ull nl = info->nlong;
+  for (ull r = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nl; r += ((ull)gridDim.x * blockDim.x) >> 5) {
+    const uint4 x = longlist[r];
+    for (uint32_t t = lane; t < x.y; t += 32) tile_k[(ull)x.x + t] = x.z;
   }
 }
 
@@ -225,111 +245,206 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   k_scan_segs<<<1, 1024, 0, s>>>(nseg, rk.seg_cnt, rk.seg_sum, rk.seg_cnt_off, rk.seg_sum_off, rk.info, rk.cumul,
                                  (ull)rk.nnz);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt_off, rk.seg_sum_off,
-                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, tile_edges);
+                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, tile_edges, rk.longlist,
+                                            rk.info);
+  k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tile_k);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ K1: frontier expansion
-// Tile of TILE = 256*E consecutive frontier edges per CTA iteration (grid-stride over tiles,
-// persistent grid sized from the SM count).  The tile's columns (<= TILE+1) are staged in
-// shared memory (edge begin within the tile, row offset); each thread maps its first edge by
-// binary search in shared memory and the next E-1 by linear advance.  The E row
-// loads are issued together, then the E visited|discovered probes (one 8-byte load each),
-// then one RED.OR per edge whose row is neither visited nor already discovered.
-template <int E>
-__global__ void __launch_bounds__(kExpandThreads) k_expand(const uint32_t* __restrict__ row,
-                                                           const uint32_t* __restrict__ flist,
-                                                           const ull* __restrict__ rowoff,
-                                                           const ull* __restrict__ cumul,
-                                                           const uint32_t* __restrict__ tile_k,
-                                                           const LevelInfo* __restrict__ info, uint32_t* vd,
-                                                           uint32_t* pmin, uint32_t col_base) {
-  constexpr int TILE = kExpandThreads * E;
+// Persistent grid, one CTA of THREADS threads per SM; every WARP independently walks warp
+// tiles of TILE = 32*E consecutive frontier edges (grid-stride), so no CTA barrier ever waits
+// on the slowest memory access.  A warp stages its tile's columns (<= TILE+1: edge begin within
+// the tile, row offset, and in P1 levels the parent's original global id) in its own shared
+// memory slice from the K3 tile table; each lane maps its first edge by binary search there and
+// the next E-1 by linear advance.  The E row loads are issued together,
+// then the visited tests: rows in the hot (relabeled, highest-degree) prefix of each row segment
+// are tested against a CTA-wide shared-memory copy of their visited bits taken at kernel start;
+// the others with one 8-byte load of the visited|discovered pair.  Then one RED.OR per row
+// neither visited nor already discovered; in P1 levels also compare-then-atomicMin of the
+// parent's global id.
+constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
+constexpr size_t kSmemBudget = 227 * 1024;
+
+template <int E, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
+                                                       const uint32_t* __restrict__ flist,
+                                                       const ull* __restrict__ rowoff,
+                                                       const ull* __restrict__ cumul,
+                                                       const uint32_t* __restrict__ tile_k,
+                                                       const LevelInfo* __restrict__ info, uint32_t* vd,
+                                                       uint32_t* pmin, const uint32_t* __restrict__ inv_col,
+                                                       uint32_t hot_words, int C, uint64_t W, int blog) {
+  constexpr int TILE = 32 * E;
+  constexpr int WARPS = THREADS / 32;
+  constexpr int SLOT = TILE + 2;
   extern __shared__ __align__(16) unsigned char smem[];
-  ull* s_off = reinterpret_cast<ull*>(smem);                        // [TILE+2]
-  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_off + TILE + 2);  // [TILE+2]
-  uint32_t* s_u = s_beg + TILE + 2;                                 // [TILE+2]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  ull* s_off = reinterpret_cast<ull*>(smem) + wid * SLOT;                                   // [SLOT]
+  uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + wid * SLOT;
+  uint32_t* s_u = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + WARPS * SLOT + wid * SLOT;
+  uint32_t* s_hot = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + 2 * WARPS * SLOT;
   const ull n = info->n, total = info->edges;
   if (total == 0) return;
   const bool p1 = info->mode == 1;
+  const uint32_t hw = (total >= kHotMinEdges && blog >= 0) ? hot_words : 0u;
+  for (uint32_t k = threadIdx.x; k < (uint32_t)C * hw; k += THREADS) {
+    const uint32_t m = k / hw, w = k - m * hw;
+    s_hot[k] = vd[2 * ((uint64_t)m * W + w)];
+  }
+  __syncthreads();
+  const uint32_t hot_bits = hw * 32;
+  const uint32_t bmask = (blog >= 0) ? ((1u << blog) - 1u) : 0u;
   const ull ntiles = (total + TILE - 1) / TILE;
-  for (ull tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const ull stride = (ull)gridDim.x * WARPS;
+  // software pipeline: the tile-table entries and the first 32 staged columns of the NEXT tile
+  // are loaded while the current tile's row loads and visited tests are in flight.
+  ull tile = (ull)blockIdx.x * WARPS + wid;
+  uint32_t klo = 0, khi = 0;
+  ull rc = 0, ro = 0;
+  uint32_t ru = 0;
+  if (tile < ntiles) {
+    klo = tile_k[tile];
+    khi = (tile + 1 < ntiles) ? tile_k[tile + 1] : (uint32_t)(n - 1);
+    if (lane <= khi - klo) {
+      rc = cumul[klo + lane];
+      ro = rowoff[klo + lane];
+      if (p1) ru = inv_col[flist[klo + lane]];
+    }
+  }
+  while (tile < ntiles) {
     const ull t0 = tile * TILE;
     const uint32_t len = (uint32_t)min((ull)TILE, total - t0);
-    const uint32_t klo = tile_k[tile];
-    const uint32_t khi = (tile + 1 < ntiles) ? tile_k[tile + 1] : (uint32_t)(n - 1);
     const uint32_t cnt = khi - klo + 1;
-    for (uint32_t idx = threadIdx.x; idx < cnt; idx += kExpandThreads) {
+    // stage this tile's columns
+    if (lane < cnt) {
+      const uint32_t beg = rc > t0 ? (uint32_t)(rc - t0) : 0u;
+      s_beg[lane] = beg;
+      s_off[lane] = ro + (t0 + beg - rc);
+      if (p1) s_u[lane] = ru;
+    }
+    for (uint32_t idx = 32 + lane; idx < cnt; idx += 32) {  // tiles of many short columns
       const ull c = cumul[klo + idx];
       const uint32_t beg = c > t0 ? (uint32_t)(c - t0) : 0u;
       s_beg[idx] = beg;
       s_off[idx] = rowoff[klo + idx] + (t0 + beg - c);
-      if (p1) s_u[idx] = flist[klo + idx];
+      if (p1) s_u[idx] = inv_col[flist[klo + idx]];
     }
-    if (threadIdx.x == 0) s_beg[cnt] = 0xFFFFFFFFu;
-    __syncthreads();
-    const uint32_t le = threadIdx.x * E;
-    if (le < len) {
-      // greatest idx < cnt with s_beg[idx] <= le (binsearch_maxle, Alg.3 line 2)
-      uint32_t lo = 0, hi = cnt - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (s_beg[mid] <= le) lo = mid; else hi = mid - 1;
+    if (lane == 0) s_beg[cnt] = 0xFFFFFFFFu;
+    __syncwarp();
+    // next tile's table entries (in flight during this tile)
+    const ull next = tile + stride;
+    uint32_t nklo = 0, nkhi = 0;
+    if (next < ntiles) {
+      nklo = tile_k[next];
+      nkhi = (next + 1 < ntiles) ? tile_k[next + 1] : (uint32_t)(n - 1);
+    }
+    // lane-interleaved edges e_q = 32q + lane: every row load instruction is one coalesced run.
+    // Lane state: the staged column idx holding its current edge, that column's end within the
+    // tile and the row-array position of tile edge 0 for that column (base + e = position).
+    uint32_t v[E], uq[E];
+    {
+      uint32_t idx = 0;
+      if (cnt > 2) {  // binsearch_maxle for the lane's first edge (Alg.3 line 2)
+        uint32_t lo = 0, hi = cnt - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_beg[mid] <= (uint32_t)lane) lo = mid; else hi = mid - 1;
+        }
+        idx = lo;
       }
-      uint32_t idx = lo;
-      uint32_t v[E], uq[E];
+      uint32_t cur_end = s_beg[idx + 1];
+      ull base = s_off[idx] - s_beg[idx];
 #pragma unroll
       for (int q = 0; q < E; ++q) {
-        const uint32_t e = le + q;
-        if (e < len) {
-          while (s_beg[idx + 1] <= e) ++idx;                              // linear advance
-          v[q] = ld_stream_u32(row + s_off[idx] + (e - s_beg[idx]));      // Alg.3 line 4
-          uq[q] = idx;
-        } else {
-          v[q] = 0xFFFFFFFFu;
+        const uint32_t e = 32u * q + lane;
+        const bool ok = e < len;
+        if (__any_sync(0xFFFFFFFFu, ok && e >= cur_end)) {  // some lane crosses a column end
+          while (ok && e >= cur_end) {                      // linear advance
+            ++idx;
+            cur_end = s_beg[idx + 1];
+            base = s_off[idx] - s_beg[idx];
+          }
         }
-      }
-      uint2 w[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) w[q] = (v[q] != 0xFFFFFFFFu) ? ld_cg_u2(vd + 2 * (v[q] >> 5)) : make_uint2(~0u, 0u);
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const uint32_t m = 1u << (v[q] & 31);
-        if (w[q].x & m) continue;  // visited (Alg.3 lines 5-6)
-        if (p1) {                  // parent claim: minimum global id (R1)
-          const uint32_t ug = col_base + s_u[uq[q]];
-          if (ug < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug);
-        }
-        if (!(w[q].y & m)) red_or(vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7 (skip if already set)
+        v[q] = ok ? ld_stream_u32(row + base + e) : 0xFFFFFFFFu;  // Alg.3 line 4
+        uq[q] = idx;
       }
     }
-    __syncthreads();
+    // hot prefix: visited at level start -> done without touching L2
+    if (hw) {
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        if (v[q] == 0xFFFFFFFFu) continue;
+        const uint32_t off = v[q] & bmask;
+        if (off < hot_bits) {
+          const uint32_t m = v[q] >> blog;
+          if ((s_hot[m * hw + (off >> 5)] >> (off & 31)) & 1u) v[q] = 0xFFFFFFFFu;
+        }
+      }
+    }
+    uint2 w[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) w[q] = (v[q] != 0xFFFFFFFFu) ? ld_cg_u2(vd + 2 * (v[q] >> 5)) : make_uint2(~0u, 0u);
+    // next tile's first 32 staged columns (in flight during the visited tests)
+    rc = 0;
+    ro = 0;
+    if (next < ntiles && lane <= nkhi - nklo) {
+      rc = cumul[nklo + lane];
+      ro = rowoff[nklo + lane];
+      if (p1) ru = inv_col[flist[nklo + lane]];
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const uint32_t m = 1u << (v[q] & 31);
+      if (w[q].x & m) continue;  // visited (Alg.3 lines 5-6)
+      if (p1) {                  // parent claim: minimum original global id (R1)
+        const uint32_t ug = s_u[uq[q]];
+        if (ug < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug);
+      }
+      if (!(w[q].y & m)) red_or(vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7 (skip if already set)
+    }
+    __syncwarp();  // all lanes done with this tile's staging
+    tile = next;
+    klo = nklo;
+    khi = nkhi;
   }
 }
 
-template <int E>
-static cudaError_t launch_expand_t(const Geom& g, Rank& rk, cudaStream_t s) {
-  constexpr int TILE = kExpandThreads * E;
-  const size_t smem = (size_t)(TILE + 2) * (8 + 4 + 4);
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(k_expand<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_expand<E>, kExpandThreads, smem);
-    if (blocks_per_sm <= 0) blocks_per_sm = 1;
+template <int E, int THREADS>
+static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cudaStream_t s) {
+  constexpr int SLOT = 32 * E + 2;
+  const size_t staging = (size_t)(THREADS / 32) * SLOT * (8 + 4 + 4);
+  // hot visited words per row segment: the relabeled prefix, as far as shared memory allows
+  int blog = -1;
+  if (g.block && (g.block & (g.block - 1)) == 0) {
+    blog = 0;
+    while ((1ull << blog) < g.block) ++blog;
   }
-  const int grid = num_sms() * blocks_per_sm;
-  k_expand<E><<<grid, kExpandThreads, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.info, rk.vd,
-                                                  rk.pmin, (uint32_t)((uint64_t)rk.j * g.ncols()));
+  uint64_t hw = hot_h / 32;
+  const uint64_t cap = (kSmemBudget - staging) / 4 / (uint64_t)g.C;
+  if (hw > cap) hw = cap;
+  if (blog < 0) hw = 0;
+  const size_t smem = staging + (size_t)g.C * hw * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_expand<E, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    attr = true;
+  }
+  k_expand<E, THREADS><<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.info,
+                                                        rk.vd, rk.pmin, rk.inv_col, (uint32_t)hw, g.C,
+                                                        g.words_block(), blog);
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(const Geom& g, Rank& rk, int E, cudaStream_t s) {
+uint32_t expand_tile_edges(int E) { return 32u * (uint32_t)E; }
+
+cudaError_t launch_expand(const Geom& g, Rank& rk, int E, uint64_t hot_h, cudaStream_t s) {
   switch (E) {
-    case 1: return launch_expand_t<1>(g, rk, s);
-    case 2: return launch_expand_t<2>(g, rk, s);
-    case 4: return launch_expand_t<4>(g, rk, s);
-    case 8: return launch_expand_t<8>(g, rk, s);
-    case 16: return launch_expand_t<16>(g, rk, s);
+    case 1: return launch_expand_t<1, 1024>(g, rk, hot_h, s);
+    case 2: return launch_expand_t<2, 1024>(g, rk, hot_h, s);
+    case 4: return launch_expand_t<4, 1024>(g, rk, hot_h, s);
+    case 8: return launch_expand_t<8, 1024>(g, rk, hot_h, s);
+    case 16: return launch_expand_t<16, 512>(g, rk, hot_h, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -350,7 +465,8 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
                                                             const ull* __restrict__ csr_ptr,
                                                             const uint32_t* __restrict__ csr_col,
                                                             const uint32_t* __restrict__ front, uint32_t* pred,
-                                                            uint32_t* pmin, uint32_t* sendbuf, uint32_t col_base,
+                                                            uint32_t* pmin, uint32_t* sendbuf,
+                                                            const uint32_t* __restrict__ inv_col,
                                                             const LevelInfo* __restrict__ info) {
   __shared__ uint32_t queue[kParentThreads / 32][1024];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -410,7 +526,7 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
           if (f[k]) best = u[k];
       }
       if (best != 0xFFFFFFFFu) {
-        pred[r] = col_base + best;
+        pred[r] = inv_col[best];
       } else {  // defer to the whole warp; slot lane+32*nlong <= q was already consumed
         queue[wid][lane + 32 * nlong] = r;
         ++nlong;
@@ -438,7 +554,7 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
             break;
           }
         }
-        if (lane == 0) pred[r] = col_base + best;
+        if (lane == 0) pred[r] = inv_col[best];
       }
     }
     __syncwarp();
@@ -452,8 +568,7 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t cap = (uint64_t)num_sms() * 4;
   if (grid > cap) grid = cap;
   k_parent<<<(unsigned)grid, kParentThreads, 0, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
-                                                     rk.pmin, g.C > 1 ? rk.sendbuf : nullptr,
-                                                     (uint32_t)((uint64_t)rk.j * g.ncols()), rk.info);
+                                                     rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info);
   return cudaGetLastError();
 }
 
@@ -518,24 +633,27 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
 // For owned t: unreached (visited bit clear) -> level -1, parent -1; reached with the winner
 // column == own column (always when C == 1) -> parent = pred of the own row segment; other
 // reached vertices are filled by the resolution exchange (k_resp_scatter).
+// t indexes the ORIGINAL owned offsets (outputs); p = fwd_own[t] the relabeled one (state).
 __global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const uint32_t* pred_own,
-                           const uint8_t* winner, int j, uint64_t block, int64_t* parent_out, int32_t* level_out) {
+                           const uint8_t* winner, const uint32_t* fwd_own, int j, uint64_t block, int64_t* parent_out,
+                           int32_t* level_out) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= block) return;
-  const bool reached = (vd_own[2 * (t >> 5)] >> (t & 31)) & 1u;
+  const uint32_t p = fwd_own[t];
+  const bool reached = (vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
   if (parent_out) {
-    int64_t p = -1;
-    if (reached && (!winner || winner[t] == (uint8_t)j)) p = (int64_t)pred_own[t];
-    parent_out[t] = p;
+    int64_t q = -1;
+    if (reached && (!winner || winner[p] == (uint8_t)j)) q = (int64_t)pred_own[p];
+    parent_out[t] = q;
   }
-  if (level_out) level_out[t] = reached ? level[t] : -1;
+  if (level_out) level_out[t] = reached ? level[p] : -1;
 }
 
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
   const unsigned grid = (unsigned)((g.block + 255) / 256);
   k_finalize<<<grid, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.level,
-                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.j, g.block,
-                                  parent_out, level_out);
+                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.fwd_own, rk.j,
+                                  g.block, parent_out, level_out);
   return cudaGetLastError();
 }
 
@@ -608,7 +726,7 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s) {
 
 // owner: scatter the answers for its requests (req_off holds the popc scan of req here)
 __global__ void k_resp_scatter(const uint32_t* req, const uint32_t* off, const uint32_t* respin, int64_t* parent,
-                               uint64_t W, uint64_t block, int C, int j) {
+                               const uint32_t* inv_own, uint64_t W, uint64_t block, int C, int j) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= W * (uint64_t)C) return;
   const int c = (int)(gid / W);
@@ -619,38 +737,44 @@ __global__ void k_resp_scatter(const uint32_t* req, const uint32_t* off, const u
   while (b) {
     const int bit = __ffs(b) - 1;
     b &= b - 1;
-    parent[w * 32 + bit] = (int64_t)respin[(uint64_t)c * block + pos++];
+    parent[inv_own[w * 32 + bit]] = (int64_t)respin[(uint64_t)c * block + pos++];
   }
 }
 
 cudaError_t launch_resp_scatter(const Geom& g, Rank& rk, int64_t* parent_out, cudaStream_t s) {
   const uint64_t W = g.words_block();
   const uint64_t n = W * g.C;
-  k_resp_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.req, rk.off_req, rk.respin, parent_out, W, g.block,
-                                                             g.C, rk.j);
+  k_resp_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.req, rk.off_req, rk.respin, parent_out, rk.inv_own,
+                                                             W, g.block, g.C, rk.j);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ m_comp, degree
-__global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uint32_t* tdeg, uint64_t block, ull* out) {
+__global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uint32_t* tdeg, const uint32_t* fwd_own,
+                                               uint64_t block, ull* out) {
   typedef cub::BlockReduce<ull, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   ull acc = 0;
   for (uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x; t < block; t += (uint64_t)gridDim.x * 256)
-    if ((vd_own[2 * (t >> 5)] >> (t & 31)) & 1u) acc += tdeg[t];
+    if ((vd_own[2 * (fwd_own[t] >> 5)] >> (fwd_own[t] & 31)) & 1u) acc += tdeg[t];
   ull tot = BR(tmp).Sum(acc);
   if (threadIdx.x == 0 && tot) atomicAdd(out, tot);
 }
 
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, ull* out, cudaStream_t s) {
-  k_mcomp<<<num_sms() * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, g.block, out);
+  k_mcomp<<<num_sms() * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, rk.fwd_own, g.block,
+                                         out);
   return cudaGetLastError();
 }
 
-__global__ void k_degree(const ull* col, uint64_t u, ull* out) { *out += col[u + 1] - col[u]; }
+// degree of ORIGINAL global vertex v held by this rank's column block (ncols columns)
+__global__ void k_degree(const ull* col, const uint32_t* perm_fwd, uint64_t v, uint64_t ncols, ull* out) {
+  const uint64_t u = (uint64_t)perm_fwd[v] % ncols;
+  *out += col[u + 1] - col[u];
+}
 
-cudaError_t launch_degree(Rank& rk, uint64_t u, ull* out, cudaStream_t s) {
-  k_degree<<<1, 1, 0, s>>>(rk.col, u, out);
+cudaError_t launch_degree(const Geom& g, Rank& rk, const uint32_t* perm_fwd, uint64_t v, ull* out, cudaStream_t s) {
+  k_degree<<<1, 1, 0, s>>>(rk.col, perm_fwd, v, g.ncols(), out);
   return cudaGetLastError();
 }
 

@@ -12,7 +12,8 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
 cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s);
 
 // K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
-cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, cudaStream_t s);
+cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, cudaStream_t s);
+uint32_t expand_tile_edges(int edges_per_thread);
 
 // K4: parent claim for the rows discovered in this level (+ pack of the fold message, C > 1).
 cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s);
@@ -37,6 +38,7 @@ cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned l
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, unsigned long long* out, cudaStream_t s);
 
 // Degree of local column u summed into *out (device u64).
-cudaError_t launch_degree(Rank& rk, uint64_t u, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_degree(const Geom& g, Rank& rk, const uint32_t* perm_fwd, uint64_t v, unsigned long long* out,
+                          cudaStream_t s);
 
 }  // namespace bfs200
