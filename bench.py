@@ -134,6 +134,34 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks_dist(x: float, world: int, device) -> float:
+    """Max of a per-rank scalar over all ranks (the step time of a multi-GPU run)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    tt = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def sample_roots_collective(n, count, degree):
+    """The first `count` distinct candidates of the root stream with degree(v) > 0.  `degree` is
+    collective (bfs_degree), so every rank walks the same candidate sequence and gets the same
+    roots."""
+    from paper_1408_1605_b200 import inputs
+    roots, seen, t = [], set(), 0
+    while len(roots) < count and t < (1 << 22):
+        v = inputs.root_candidate(inputs.ROOT_SEED, t, n)
+        t += 1
+        if v in seen:
+            continue
+        seen.add(v)
+        if degree(v) > 0:
+            roots.append(v)
+    return roots
+
+
 def workload_config(args, world):
     R, C = GRIDS.get(world, (1, world))
     scale = args.scale if args.scale else 26 + int(round(math.log2(world)))
@@ -177,13 +205,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
     info = g.info
     # 64 timed roots + W warm-up roots: degree >= 1, distinct, root stream of seed 2
-    need = 64 + args.warmup
-    roots, t = [], 0
-    while len(roots) < need and t < (1 << 22):
-        v = inputs.root_candidate(inputs.ROOT_SEED, t, n)
-        t += 1
-        if v not in roots and g.degree(v) > 0:
-            roots.append(v)
+    roots = sample_roots_collective(n, 64 + args.warmup, g.degree)
     timed_roots = roots[:64]
     warm_roots = roots[64:] or roots[:1]
     parent = torch.empty(info.nout, dtype=torch.int64, device=dev)
@@ -197,11 +219,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        tt = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return max_over_ranks_dist(x, world, dev)
 
     for k in range(args.warmup):
         g.run(warm_roots[k % len(warm_roots)], parent, level)

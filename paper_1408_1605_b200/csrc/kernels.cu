@@ -43,6 +43,21 @@ __device__ __forceinline__ void red_or(uint32_t* p, uint32_t m) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(m) : "memory");
 }
 
+// predicated forms (no branch, no reconvergence point): the destination keeps its input value
+// when the predicate is false
+__device__ __forceinline__ void ld_stream_u32_if(bool p, const uint32_t* a, uint32_t& v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
+               : "+r"(v) : "l"(a), "r"((int)p));
+}
+__device__ __forceinline__ void ld_cg_u2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
+               : "+r"(x), "+r"(y) : "l"(a), "r"((int)p));
+}
+__device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q red.relaxed.gpu.global.or.b32 [%0], %1; }"
+               ::"l"(a), "r"(m), "r"((int)p) : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
                                                              uint64_t nseg, const ull* __restrict__ col,
                                                              const uint32_t* cnt_off, const ull* sum_off,
                                                              uint32_t* flist, ull* rowoff, ull* cumul,
-                                                             uint32_t* tile_k, uint32_t tile_edges, uint4* longlist,
+                                                             uint32_t* tile_k, int tile_shift, uint4* longlist,
                                                              LevelInfo* info) {
   const int lane = threadIdx.x & 31;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
@@ -213,7 +228,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         flist[pos] = (uint32_t)u;
         rowoff[pos] = c0;
         cumul[pos] = eb;
-        const ull tf = (eb + tile_edges - 1) / tile_edges, tl = (eb + d + tile_edges - 1) / tile_edges;
+        const ull tm = (1ull << tile_shift) - 1;  // tiles are 2^tile_shift edges
+        const ull tf = (eb + tm) >> tile_shift, tl = (eb + d + tm) >> tile_shift;
         if (tl - tf <= 8) {
           for (ull t = tf; t < tl; ++t) tile_k[t] = (uint32_t)pos;
         } else {  // long column: the tile-table range is filled by k_tile_fill
@@ -245,7 +261,7 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   k_scan_segs<<<1, 1024, 0, s>>>(nseg, rk.seg_cnt, rk.seg_sum, rk.seg_cnt_off, rk.seg_sum_off, rk.info, rk.cumul,
                                  (ull)rk.nnz);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt_off, rk.seg_sum_off,
-                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, tile_edges, rk.longlist,
+                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, __builtin_ctz(tile_edges), rk.longlist,
                                             rk.info);
   k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tile_k);
   return cudaGetLastError();
@@ -266,31 +282,62 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
 
-template <int E, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
-                                                       const uint32_t* __restrict__ flist,
-                                                       const ull* __restrict__ rowoff,
-                                                       const ull* __restrict__ cumul,
-                                                       const uint32_t* __restrict__ tile_k,
-                                                       const LevelInfo* __restrict__ info, uint32_t* vd,
-                                                       uint32_t* pmin, const uint32_t* __restrict__ inv_col,
-                                                       uint32_t hot_words, int C, uint64_t W, int blog) {
+// One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
+// against the shared-memory copy, the others with one 8-byte load of the visited|discovered
+// pair), then the discovered bit by RED.OR and, in P1 levels, the parent claim.
+template <int WV, bool P1>
+__device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vd,
+                                             uint32_t* pmin, const uint32_t* s_hot, uint32_t hot_bits,
+                                             uint32_t bmask, int blog, uint32_t hw) {
+  uint32_t wx[WV], wy[WV];
+#pragma unroll
+  for (int q = 0; q < WV; ++q) {
+    const bool ok = v[q] != 0xFFFFFFFFu;
+    bool need = ok;
+    if (!P1) {
+      const uint32_t off = v[q] & bmask;
+      const bool inhot = ok && off < hot_bits;
+      const uint32_t hword = s_hot[inhot ? (v[q] >> blog) * hw + (off >> 5) : 0u];
+      need = ok && !(inhot && ((hword >> (off & 31)) & 1u));
+    }
+    wx[q] = 0xFFFFFFFFu;
+    wy[q] = 0xFFFFFFFFu;
+    ld_cg_u2_if(need, vd + 2 * (v[q] >> 5), wx[q], wy[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < WV; ++q) {
+    const uint32_t m = 1u << (v[q] & 31);
+    const bool cand = !(wx[q] & m);  // not visited (Alg.3 lines 5-6)
+    if (P1 && cand) {                // parent claim: minimum original global id (R1)
+      if (ug[q] < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug[q]);
+    }
+    red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+  }
+}
+
+template <int E, int THREADS, bool P1>
+__device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
+                                            const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
+                                            const uint32_t* __restrict__ tile_k, ull n, ull total, uint32_t* vd,
+                                            uint32_t* pmin, const uint32_t* __restrict__ inv_col, uint32_t hot_words,
+                                            int C, uint64_t W, int blog) {
   constexpr int TILE = 32 * E;
   constexpr int WARPS = THREADS / 32;
   constexpr int SLOT = TILE + 2;
+  constexpr int WV = E < 4 ? E : 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  ull* s_off = reinterpret_cast<ull*>(smem) + wid * SLOT;                                   // [SLOT]
+  ull* s_off = reinterpret_cast<ull*>(smem) + wid * SLOT;
   uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + wid * SLOT;
-  uint32_t* s_u = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + WARPS * SLOT + wid * SLOT;
-  uint32_t* s_hot = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + 2 * WARPS * SLOT;
-  const ull n = info->n, total = info->edges;
-  if (total == 0) return;
-  const bool p1 = info->mode == 1;
-  const uint32_t hw = (total >= kHotMinEdges && blog >= 0) ? hot_words : 0u;
+  // the region after the staging holds either the parents' ids (P1) or the hot visited bits
+  uint32_t* s_region = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + WARPS * SLOT;
+  uint32_t* s_u = s_region + wid * SLOT;
+  const uint32_t* s_hot = s_region;
+  uint32_t hw = 0;
+  if (!P1 && total >= kHotMinEdges && blog >= 0) hw = hot_words;
   for (uint32_t k = threadIdx.x; k < (uint32_t)C * hw; k += THREADS) {
     const uint32_t m = k / hw, w = k - m * hw;
-    s_hot[k] = vd[2 * ((uint64_t)m * W + w)];
+    s_region[k] = vd[2 * ((uint64_t)m * W + w)];
   }
   __syncthreads();
   const uint32_t hot_bits = hw * 32;
@@ -309,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
     if (lane <= khi - klo) {
       rc = cumul[klo + lane];
       ro = rowoff[klo + lane];
-      if (p1) ru = inv_col[flist[klo + lane]];
+      if (P1) ru = inv_col[flist[klo + lane]];
     }
   }
   while (tile < ntiles) {
@@ -321,14 +368,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
       const uint32_t beg = rc > t0 ? (uint32_t)(rc - t0) : 0u;
       s_beg[lane] = beg;
       s_off[lane] = ro + (t0 + beg - rc);
-      if (p1) s_u[lane] = ru;
+      if (P1) s_u[lane] = ru;
     }
     for (uint32_t idx = 32 + lane; idx < cnt; idx += 32) {  // tiles of many short columns
       const ull c = cumul[klo + idx];
       const uint32_t beg = c > t0 ? (uint32_t)(c - t0) : 0u;
       s_beg[idx] = beg;
       s_off[idx] = rowoff[klo + idx] + (t0 + beg - c);
-      if (p1) s_u[idx] = inv_col[flist[klo + idx]];
+      if (P1) s_u[idx] = inv_col[flist[klo + idx]];
     }
     if (lane == 0) s_beg[cnt] = 0xFFFFFFFFu;
     __syncwarp();
@@ -339,11 +386,63 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
       nklo = tile_k[next];
       nkhi = (next + 1 < ntiles) ? tile_k[next + 1] : (uint32_t)(n - 1);
     }
-    // lane-interleaved edges e_q = 32q + lane: every row load instruction is one coalesced run.
-    // Lane state: the staged column idx holding its current edge, that column's end within the
-    // tile and the row-array position of tile edge 0 for that column (base + e = position).
-    uint32_t v[E], uq[E];
-    {
+    bool rnext = false;
+    auto prefetch_next = [&]() {  // next tile's first 32 staged columns
+      if (next < ntiles && lane <= nkhi - nklo) {
+        rc = cumul[nklo + lane];
+        ro = rowoff[nklo + lane];
+        if (P1) ru = inv_col[flist[nklo + lane]];
+        rnext = true;
+      }
+    };
+    if (!P1 && cnt == 1 && len == TILE) {
+      // lean path (the bulk of a dense level): a full tile inside one column, positions base + e,
+      // every lane valid; branch-free visited test, predicated probe and RED.
+      const uint32_t* rp = row + s_off[0] + lane;
+      const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
+      const int bl = blog > 0 ? blog : 0;
+#pragma unroll
+      for (int wv = 0; wv < E / WV; ++wv) {
+        uint32_t v[WV];
+#pragma unroll
+        for (int q = 0; q < WV; ++q) v[q] = ld_stream_u32(rp + 32 * (WV * wv + q));  // Alg.3 line 4
+        if (wv == 0) prefetch_next();
+        uint32_t x[WV], y[WV];
+#pragma unroll
+        for (int q = 0; q < WV; ++q) {
+          const uint32_t off = v[q] & bmask;
+          const uint32_t hword = s_hot[(v[q] >> bl) * hw + (min(off, hclamp) >> 5)];
+          const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
+          x[q] = 0xFFFFFFFFu;
+          y[q] = 0xFFFFFFFFu;
+          ld_cg_u2_if(!hv, vd + 2 * (v[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
+        }
+#pragma unroll
+        for (int q = 0; q < WV; ++q) {
+          const uint32_t m = 1u << (v[q] & 31);
+          red_or_if(!((x[q] | y[q]) & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+        }
+      }
+    } else if (cnt == 1) {
+      // the whole tile lies in one column: positions are base + e, no mapping work
+      const ull base = s_off[0];
+      const uint32_t u0 = P1 ? s_u[0] : 0u;
+#pragma unroll
+      for (int wv = 0; wv < E / WV; ++wv) {
+        uint32_t v[WV], ug[WV];
+#pragma unroll
+        for (int q = 0; q < WV; ++q) {
+          const uint32_t e = 32u * (WV * wv + q) + lane;
+          v[q] = 0xFFFFFFFFu;
+          ld_stream_u32_if(e < len, row + base + e, v[q]);  // Alg.3 line 4
+          ug[q] = u0;
+        }
+        if (wv == 0) prefetch_next();
+        expand_edges<WV, P1>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+      }
+    } else {
+      // lane-interleaved edges e = 32q + lane; lane state: the staged column idx holding its
+      // current edge, that column's end within the tile and base = row position of tile edge 0
       uint32_t idx = 0;
       if (cnt > 2) {  // binsearch_maxle for the lane's first edge (Alg.3 line 2)
         uint32_t lo = 0, hi = cnt - 1;
@@ -352,56 +451,36 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
           if (s_beg[mid] <= (uint32_t)lane) lo = mid; else hi = mid - 1;
         }
         idx = lo;
+      } else {
+        idx = (uint32_t)lane >= s_beg[1] ? 1u : 0u;
       }
       uint32_t cur_end = s_beg[idx + 1];
       ull base = s_off[idx] - s_beg[idx];
 #pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const uint32_t e = 32u * q + lane;
-        const bool ok = e < len;
-        if (__any_sync(0xFFFFFFFFu, ok && e >= cur_end)) {  // some lane crosses a column end
-          while (ok && e >= cur_end) {                      // linear advance
-            ++idx;
-            cur_end = s_beg[idx + 1];
-            base = s_off[idx] - s_beg[idx];
+      for (int wv = 0; wv < E / WV; ++wv) {
+        uint32_t v[WV], ug[WV];
+#pragma unroll
+        for (int q = 0; q < WV; ++q) {
+          const uint32_t e = 32u * (WV * wv + q) + lane;
+          const bool ok = e < len;
+          if (__any_sync(0xFFFFFFFFu, ok && e >= cur_end)) {  // some lane crosses a column end
+            while (ok && e >= cur_end) {                      // linear advance
+              ++idx;
+              cur_end = s_beg[idx + 1];
+              base = s_off[idx] - s_beg[idx];
+            }
           }
+          v[q] = 0xFFFFFFFFu;
+          ld_stream_u32_if(ok, row + base + e, v[q]);  // Alg.3 line 4
+          ug[q] = P1 ? s_u[idx] : 0u;
         }
-        v[q] = ok ? ld_stream_u32(row + base + e) : 0xFFFFFFFFu;  // Alg.3 line 4
-        uq[q] = idx;
+        if (wv == 0) prefetch_next();
+        expand_edges<WV, P1>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
       }
     }
-    // hot prefix: visited at level start -> done without touching L2
-    if (hw) {
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        if (v[q] == 0xFFFFFFFFu) continue;
-        const uint32_t off = v[q] & bmask;
-        if (off < hot_bits) {
-          const uint32_t m = v[q] >> blog;
-          if ((s_hot[m * hw + (off >> 5)] >> (off & 31)) & 1u) v[q] = 0xFFFFFFFFu;
-        }
-      }
-    }
-    uint2 w[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) w[q] = (v[q] != 0xFFFFFFFFu) ? ld_cg_u2(vd + 2 * (v[q] >> 5)) : make_uint2(~0u, 0u);
-    // next tile's first 32 staged columns (in flight during the visited tests)
-    rc = 0;
-    ro = 0;
-    if (next < ntiles && lane <= nkhi - nklo) {
-      rc = cumul[nklo + lane];
-      ro = rowoff[nklo + lane];
-      if (p1) ru = inv_col[flist[nklo + lane]];
-    }
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const uint32_t m = 1u << (v[q] & 31);
-      if (w[q].x & m) continue;  // visited (Alg.3 lines 5-6)
-      if (p1) {                  // parent claim: minimum original global id (R1)
-        const uint32_t ug = s_u[uq[q]];
-        if (ug < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug);
-      }
-      if (!(w[q].y & m)) red_or(vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7 (skip if already set)
+    if (!rnext) {
+      rc = 0;
+      ro = 0;
     }
     __syncwarp();  // all lanes done with this tile's staging
     tile = next;
@@ -411,9 +490,30 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
 }
 
 template <int E, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
+                                                       const uint32_t* __restrict__ flist,
+                                                       const ull* __restrict__ rowoff,
+                                                       const ull* __restrict__ cumul,
+                                                       const uint32_t* __restrict__ tile_k,
+                                                       const LevelInfo* __restrict__ info, uint32_t* vd,
+                                                       uint32_t* pmin, const uint32_t* __restrict__ inv_col,
+                                                       uint32_t hot_words, int C, uint64_t W, int blog) {
+  const ull n = info->n, total = info->edges;
+  if (total == 0) return;
+  if (info->mode == 1)
+    expand_body<E, THREADS, true>(row, flist, rowoff, cumul, tile_k, n, total, vd, pmin, inv_col, hot_words, C, W,
+                                  blog);
+  else
+    expand_body<E, THREADS, false>(row, flist, rowoff, cumul, tile_k, n, total, vd, pmin, inv_col, hot_words, C, W,
+                                   blog);
+}
+
+template <int E, int THREADS>
 static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cudaStream_t s) {
   constexpr int SLOT = 32 * E + 2;
-  const size_t staging = (size_t)(THREADS / 32) * SLOT * (8 + 4 + 4);
+  constexpr size_t WARPS = THREADS / 32;
+  const size_t staging = WARPS * SLOT * (8 + 4);
+  const size_t s_u_bytes = WARPS * SLOT * 4;
   // hot visited words per row segment: the relabeled prefix, as far as shared memory allows
   int blog = -1;
   if (g.block && (g.block & (g.block - 1)) == 0) {
@@ -421,10 +521,12 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
     while ((1ull << blog) < g.block) ++blog;
   }
   uint64_t hw = hot_h / 32;
-  const uint64_t cap = (kSmemBudget - staging) / 4 / (uint64_t)g.C;
+  const uint64_t cap = (kSmemBudget - staging - 16) / 4 / (uint64_t)g.C;
   if (hw > cap) hw = cap;
   if (blog < 0) hw = 0;
-  const size_t smem = staging + (size_t)g.C * hw * 4;
+  size_t region = (size_t)g.C * hw * 4;
+  if (region < s_u_bytes) region = s_u_bytes;
+  const size_t smem = staging + region + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_expand<E, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
@@ -580,11 +682,12 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
 __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* recv, uint32_t* front_seg,
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
                                                 int j, int lvl) {
-  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // grid: x over the words of one segment, y = segment m (no 64-bit division)
+  const int m = (int)blockIdx.y;
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gid = (uint64_t)m * W + w;
   uint32_t newbits = 0;
-  if (gid < W * (uint64_t)C) {
-    const int m = (int)(gid / W);
-    const uint64_t w = gid - (uint64_t)m * W;
+  if (w < W) {
     uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
     if (m != j) {
       if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
@@ -622,8 +725,7 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
 
 cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
   const uint64_t W = g.words_block();
-  const uint64_t nthreads = W * (uint64_t)g.C;
-  const unsigned grid = (unsigned)((nthreads + 255) / 256);
+  const dim3 grid((unsigned)((W + 255) / 256), (unsigned)g.C);
   k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
                                 g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, lvl);
   return cudaGetLastError();
