@@ -21,13 +21,17 @@ constexpr int kMaxLevels = 4096;
 // Device-side per-level counters written by the scan kernels (read by the expansion kernel,
 // so the host never needs the frontier size to launch it).
 struct LevelInfo {
-  unsigned long long n;      // frontier columns with local degree > 0
-  unsigned long long edges;  // cumul[n]
-  unsigned long long newv;   // vertices discovered by the update (this rank)
-  unsigned long long mode;   // parent claim of this level: 1 = atomicMin in the expansion (P1),
-                             // 2 = CSR scan of the discovered rows (P2); see k_scan_segs
-  unsigned long long nlong;  // long columns whose tile-table range is filled by k_tile_fill
-  unsigned long long pad[3];
+  unsigned long long n;       // short frontier columns (0 < local degree < TILE/2), listed in flist
+  unsigned long long edges;   // all CSC entries leaving the frontier (short + long)
+  unsigned long long newv;    // vertices discovered by the update (this rank)
+  unsigned long long mode;    // parent claim of this level: 1 = atomicMin in the expansion (P1),
+                              // 2 = CSR scan of the discovered rows (P2); see k_scan_segs
+  unsigned long long nlong;   // hub columns whose long-tile records are written by k_tile_fill
+  unsigned long long sedges;  // edges of the short columns = cumul[n]
+  unsigned long long nA;      // long-column tiles (tileA records)
+  unsigned long long ncols;   // short columns (stats)
+  unsigned long long nlongcols;  // long columns (stats)
+  unsigned long long pad[7];
 };
 
 // Geometry of the 2D partition (index maps SPEC.md S:109-148).
@@ -71,11 +75,10 @@ struct Rank {
   unsigned long long* rowoff = nullptr;  // [ncols] col[flist[k]]
   unsigned long long* cumul = nullptr;   // [ncols+1] exclusive scan of degrees
   uint32_t* tile_k = nullptr;            // [nnz/32 + 2] first frontier index of every expansion tile
-  uint4* longlist = nullptr;             // [nnz/128 + 64] (first tile, #tiles, column index) of long columns
-  uint32_t* seg_cnt = nullptr;           // [nseg] per-segment frontier count (degree > 0)
-  unsigned long long* seg_sum = nullptr; // [nseg] per-segment degree sum
-  uint32_t* seg_cnt_off = nullptr;       // exclusive scans of the above
-  unsigned long long* seg_sum_off = nullptr;
+  uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
+  void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
+  void* seg_off = nullptr;               // [nseg] their exclusive scan
+  uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution
   int32_t* level_tmp = nullptr;          // [block] level staging for host outputs

@@ -188,12 +188,11 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.flist, g.ncols() * 4);
   AL(rk.rowoff, g.ncols() * 8);
   AL(rk.cumul, (g.ncols() + 1) * 8);
-  AL(rk.tile_k, (rk.nnz / 32 + 2) * 4);  // expansion tiles have >= 32 edges
-  AL(rk.longlist, (rk.nnz / 128 + 64) * 16);  // a long column spans > 8 tiles of >= 32 edges
-  AL(rk.seg_cnt, nseg * 4);
-  AL(rk.seg_sum, nseg * 8);
-  AL(rk.seg_cnt_off, nseg * 4);
-  AL(rk.seg_sum_off, nseg * 8);
+  AL(rk.tile_k, (rk.nnz / 32 + 2) * 4);          // short-edge tiles have >= 32 edges
+  AL(rk.tileA, (3 * (rk.nnz / 32) + 64) * 16);    // long tiles: <= nnz/TILE + #long columns (d >= TILE/2)
+  AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
+  AL(rk.seg_tot, nseg * 24);
+  AL(rk.seg_off, nseg * 24);
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
   AL(rk.scratch, 64 * 8);
@@ -448,7 +447,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     ull total_new = 0, fr = 0, ed = 0;
     for (size_t k = 0; k < G.ranks.size(); ++k) {
       total_new += G.h_infos[k].newv;
-      fr += G.h_infos[k].n;
+      fr += G.h_infos[k].n + G.h_infos[k].nlongcols;
       ed += G.h_infos[k].edges;
     }
     G.lvl_frontier.push_back(fr);

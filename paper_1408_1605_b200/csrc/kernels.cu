@@ -28,7 +28,7 @@ typedef unsigned long long ull;
 // ------------------------------------------------------------------ small helpers
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 
@@ -46,16 +46,16 @@ __device__ __forceinline__ void red_or(uint32_t* p, uint32_t m) {
 // predicated forms (no branch, no reconvergence point): the destination keeps its input value
 // when the predicate is false
 __device__ __forceinline__ void ld_stream_u32_if(bool p, const uint32_t* a, uint32_t& v) {
-  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
                : "+r"(v) : "l"(a), "r"((int)p));
 }
 __device__ __forceinline__ void ld_cg_u2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
-  asm volatile("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
+  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
                : "+r"(x), "+r"(y) : "l"(a), "r"((int)p));
 }
 __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q red.relaxed.gpu.global.or.b32 [%0], %1; }"
-               ::"l"(a), "r"(m), "r"((int)p) : "memory");
+               ::"l"(a), "r"(m), "r"((int)p));
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -102,18 +102,38 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
 }
 
 // ------------------------------------------------------------------ K3: unpack + degree scan
-// A warp owns a segment of kScanSegWords bitmap words; it walks the non-zero words 32 at a
-// time and, per word, lane b handles bit b, so the col[] reads of one word are coalesced.
+// Frontier columns are split by degree d (E = edges per thread, TILE = 32*E):
+//   short (0 < d < TILE/2): listed in ascending order with their row offsets and the exclusive
+//     scan of their degrees `cumul`; the expansion maps threads to their edges by
+//     the scan + binary search of P:455-470 over tiles of TILE consecutive short edges, and K3
+//     also emits the first column of every such tile (tile_k);
+//   long (d >= TILE/2): cut into ceil(d/TILE) column-aligned tiles whose (row position, length,
+//     column) records are emitted directly (tileA): the mapping of those edges is the identity
+//     inside one column, which is where almost all edges of a dense level live.
+// A warp owns a segment of kScanSegWords bitmap words; it walks the non-zero words 32 at a time
+// and, per word, lane b handles bit b, so the col[] reads of one word are coalesced.
+struct SegTot {
+  unsigned int cs;  // short columns
+  unsigned int na;  // long-column tiles
+  ull ss;           // short edges
+  ull ls;           // long edges
+};
+struct SegAdd {
+  __device__ __forceinline__ SegTot operator()(const SegTot& a, const SegTot& b) const {
+    return SegTot{a.cs + b.cs, a.na + b.na, a.ss + b.ss, a.ls + b.ls};
+  }
+};
+
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                               uint64_t nseg, const ull* __restrict__ col,
-                                                              uint32_t* seg_cnt, ull* seg_sum) {
+                                                              SegTot* seg_tot, int tile_shift) {
   const int lane = threadIdx.x & 31;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
   if (seg >= nseg) return;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
-  unsigned cnt = 0;
-  ull sum = 0;
+  const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
+  SegTot t{0u, 0u, 0ull, 0ull};
   for (uint64_t wb = w0; wb < w1; wb += 32) {
     const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
     unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
@@ -124,84 +144,81 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
       if ((xw >> lane) & 1u) {
         const uint64_t u = (wb + jw) * 32 + lane;
         const ull d = __ldg(col + u + 1) - __ldg(col + u);
-        cnt += d ? 1u : 0u;
-        sum += d;
+        if (d >= half) {
+          t.na += (unsigned)((d + tm) >> tile_shift);
+          t.ls += d;
+        } else if (d) {
+          t.cs += 1u;
+          t.ss += d;
+        }
       }
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    t.cs += __shfl_xor_sync(0xFFFFFFFFu, t.cs, o);
+    t.na += __shfl_xor_sync(0xFFFFFFFFu, t.na, o);
+    t.ss += __shfl_xor_sync(0xFFFFFFFFu, t.ss, o);
+    t.ls += __shfl_xor_sync(0xFFFFFFFFu, t.ls, o);
   }
-  if (lane == 0) {
-    seg_cnt[seg] = cnt;
-    seg_sum[seg] = sum;
-  }
+  if (lane == 0) seg_tot[seg] = t;
 }
 
-struct CS {
-  unsigned int c;
-  ull s;
-};
-struct CSAdd {
-  __device__ __forceinline__ CS operator()(const CS& a, const CS& b) const { return CS{a.c + b.c, a.s + b.s}; }
-};
-
-// exclusive scan over segments (one CTA); writes n, edges, cumul[n]; resets the update counter
-__global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const uint32_t* seg_cnt, const ull* seg_sum,
-                                                    uint32_t* cnt_off, ull* sum_off, LevelInfo* info, ull* cumul,
-                                                    ull nnz) {
-  typedef cub::BlockScan<CS, 1024> BS;
+// exclusive scan over segments (one CTA); writes the level totals, cumul[n]; resets counters
+__global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const SegTot* seg_tot, SegTot* seg_off,
+                                                    LevelInfo* info, ull* cumul, ull nnz) {
+  typedef cub::BlockScan<SegTot, 1024> BS;
   __shared__ typename BS::TempStorage tmp;
-  __shared__ CS carry;
-  if (threadIdx.x == 0) carry = CS{0u, 0ull};
+  __shared__ SegTot carry;
+  if (threadIdx.x == 0) carry = SegTot{0u, 0u, 0ull, 0ull};
   __syncthreads();
   for (uint64_t base = 0; base < nseg; base += 1024) {
     const uint64_t t = base + threadIdx.x;
-    CS v = (t < nseg) ? CS{seg_cnt[t], seg_sum[t]} : CS{0u, 0ull};
-    CS ex, agg;
-    BS(tmp).ExclusiveScan(v, ex, CS{0u, 0ull}, CSAdd(), agg);
-    const CS c0 = carry;
-    if (t < nseg) {
-      cnt_off[t] = c0.c + ex.c;
-      sum_off[t] = c0.s + ex.s;
-    }
+    SegTot v = (t < nseg) ? seg_tot[t] : SegTot{0u, 0u, 0ull, 0ull};
+    SegTot ex, agg;
+    BS(tmp).ExclusiveScan(v, ex, SegTot{0u, 0u, 0ull, 0ull}, SegAdd(), agg);
+    const SegTot c0 = carry;
+    if (t < nseg) seg_off[t] = SegAdd()(c0, ex);
     __syncthreads();
-    if (threadIdx.x == 0) carry = CS{c0.c + agg.c, c0.s + agg.s};
+    if (threadIdx.x == 0) carry = SegAdd()(c0, agg);
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    info->n = carry.c;
-    info->edges = carry.s;
+    const SegTot c = carry;
+    info->n = c.cs;
+    info->sedges = c.ss;
+    info->nA = c.na;
+    info->edges = c.ss + c.ls;
+    info->ncols = c.cs + 0ull;  // long columns are counted by k_scan_emit (info->nlongcols)
     info->newv = 0;
     // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
     // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
     // the scan (P2) is used when that is <= 4; otherwise (small frontiers, e.g. the first
     // levels) the expansion does compare-then-atomicMin per candidate edge (P1).
-    info->mode = (carry.s * 4ull >= nnz) ? 2ull : 1ull;
+    info->mode = ((c.ss + c.ls) * 4ull >= nnz) ? 2ull : 1ull;
     info->nlong = 0;
-    cumul[carry.c] = carry.s;
+    info->nlongcols = 0;
+    cumul[c.cs] = c.ss;
   }
 }
 
-// emit the frontier list (columns with degree > 0, ascending), their row offsets, the
-// exclusive degree scan cumul, and for every expansion tile starting inside a column's edge
-// range the index of that column (tile_k): the thread->edge mapping table.
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                              uint64_t nseg, const ull* __restrict__ col,
-                                                             const uint32_t* cnt_off, const ull* sum_off,
-                                                             uint32_t* flist, ull* rowoff, ull* cumul,
-                                                             uint32_t* tile_k, int tile_shift, uint4* longlist,
-                                                             LevelInfo* info) {
+                                                             const SegTot* seg_off, uint32_t* flist, ull* rowoff,
+                                                             ull* cumul, uint32_t* tile_k, uint4* tileA,
+                                                             int tile_shift, uint4* longlist, LevelInfo* info) {
   const int lane = threadIdx.x & 31;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
   if (seg >= nseg) return;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
-  uint64_t k = cnt_off[seg];
-  ull e = sum_off[seg];
+  const SegTot o = seg_off[seg];
+  uint64_t k = o.cs;  // next short list position
+  ull e = o.ss;       // next short edge position
+  uint64_t a = o.na;  // next long-tile position
+  const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   const unsigned lt = lanemask_lt();
+  unsigned nlongcols = 0;
   for (uint64_t wb = w0; wb < w1; wb += 32) {
     const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
     unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
@@ -215,41 +232,69 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         c0 = __ldg(col + u);
         d = __ldg(col + u + 1) - c0;
       }
-      const unsigned mask = __ballot_sync(0xFFFFFFFFu, d != 0);
-      ull inc = d;  // inclusive warp scan of degrees
+      const bool isl = d >= half;
+      const ull ds = isl ? 0ull : d;
+      const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
+      const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
+      ull inc = ds;     // inclusive warp scan of short degrees
+      unsigned ia = na; // inclusive warp scan of long-tile counts
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= o) inc += y;
+      for (int s2 = 1; s2 < 32; s2 <<= 1) {
+        const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
+        const unsigned ya = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
+        if (lane >= s2) {
+          inc += y;
+          ia += ya;
+        }
       }
-      if (d) {
-        const uint64_t pos = k + __popc(mask & lt);
-        const ull eb = e + inc - d;
+      if (ds) {
+        const uint64_t pos = k + __popc(smask & lt);
+        const ull eb = e + inc - ds;
         flist[pos] = (uint32_t)u;
         rowoff[pos] = c0;
         cumul[pos] = eb;
-        const ull tm = (1ull << tile_shift) - 1;  // tiles are 2^tile_shift edges
-        const ull tf = (eb + tm) >> tile_shift, tl = (eb + d + tm) >> tile_shift;
-        if (tl - tf <= 8) {
-          for (ull t = tf; t < tl; ++t) tile_k[t] = (uint32_t)pos;
-        } else {  // long column: the tile-table range is filled by k_tile_fill
-          const ull slot = atomicAdd(&info->nlong, 1ull);
-          longlist[slot] = make_uint4((uint32_t)tf, (uint32_t)(tl - tf), (uint32_t)pos, 0u);
-        }
+        // a short column spans at most two tiles
+        for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
       }
-      k += __popc(mask);
+      if (isl) {
+        const uint64_t pa = a + ia - na;
+        if (na <= 8) {
+          for (unsigned q = 0; q < na; ++q) {
+            const ull pos = c0 + ((ull)q << tile_shift);
+            const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+            tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
+          }
+        } else {  // hub column: its tiles are written by k_tile_fill
+          const ull slot = atomicAdd(&info->nlong, 1ull);
+          longlist[2 * slot] = make_uint4((uint32_t)pa, na, (uint32_t)u, (uint32_t)(pa >> 32));
+          longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
+        }
+        ++nlongcols;
+      }
+      k += __popc(smask);
       e += __shfl_sync(0xFFFFFFFFu, inc, 31);
+      a += __shfl_sync(0xFFFFFFFFu, ia, 31);
     }
   }
+#pragma unroll
+  for (int s2 = 16; s2; s2 >>= 1) nlongcols += __shfl_xor_sync(0xFFFFFFFFu, nlongcols, s2);
+  if (lane == 0 && nlongcols) atomicAdd(&info->nlongcols, (ull)nlongcols);
 }
 
-// tile-table ranges of long columns: one warp per range
-__global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint32_t* tile_k) {
+// long-tile records of hub columns: one warp per column
+__global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4* tileA, int tile_shift) {
   const int lane = threadIdx.x & 31;
   const ull nl = info->nlong;
+  const ull tm = (1ull << tile_shift) - 1;
   for (ull r = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nl; r += ((ull)gridDim.x * blockDim.x) >> 5) {
-    const uint4 x = longlist[r];
-    for (uint32_t t = lane; t < x.y; t += 32) tile_k[(ull)x.x + t] = x.z;
+    const uint4 h = longlist[2 * r], b = longlist[2 * r + 1];
+    const ull pa = (ull)h.x | ((ull)h.w << 32);
+    const ull c0 = (ull)b.x | ((ull)b.y << 32), d = (ull)b.z | ((ull)b.w << 32);
+    for (uint32_t q = lane; q < h.y; q += 32) {
+      const ull pos = c0 + ((ull)q << tile_shift);
+      const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+      tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, h.z);
+    }
   }
 }
 
@@ -257,13 +302,14 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   const uint64_t nwords = g.ncols() / 32;
   const uint64_t nseg = (nwords + kScanSegWords - 1) / kScanSegWords;
   const unsigned grid = (unsigned)((nseg + kScanThreads / 32 - 1) / (kScanThreads / 32));
-  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt, rk.seg_sum);
-  k_scan_segs<<<1, 1024, 0, s>>>(nseg, rk.seg_cnt, rk.seg_sum, rk.seg_cnt_off, rk.seg_sum_off, rk.info, rk.cumul,
-                                 (ull)rk.nnz);
-  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.seg_cnt_off, rk.seg_sum_off,
-                                            rk.flist, rk.rowoff, rk.cumul, rk.tile_k, __builtin_ctz(tile_edges), rk.longlist,
-                                            rk.info);
-  k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tile_k);
+  const int ts = __builtin_ctz(tile_edges);
+  SegTot* st = static_cast<SegTot*>(rk.seg_tot);
+  SegTot* so = static_cast<SegTot*>(rk.seg_off);
+  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
+  k_scan_segs<<<1, 1024, 0, s>>>(nseg, st, so, rk.info, rk.cumul, (ull)rk.nnz);
+  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
+                                            rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
+  k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
   return cudaGetLastError();
 }
 
@@ -308,9 +354,7 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
   for (int q = 0; q < WV; ++q) {
     const uint32_t m = 1u << (v[q] & 31);
     const bool cand = !(wx[q] & m);  // not visited (Alg.3 lines 5-6)
-    if (P1 && cand) {                // parent claim: minimum original global id (R1)
-      if (ug[q] < *(volatile uint32_t*)(pmin + v[q])) atomicMin(pmin + v[q], ug[q]);
-    }
+    if (P1 && cand) atomicMin(pmin + v[q], ug[q]);  // parent claim: minimum original id (R1)
     red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
   }
 }
@@ -318,9 +362,10 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 template <int E, int THREADS, bool P1>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
                                             const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
-                                            const uint32_t* __restrict__ tile_k, ull n, ull total, uint32_t* vd,
-                                            uint32_t* pmin, const uint32_t* __restrict__ inv_col, uint32_t hot_words,
-                                            int C, uint64_t W, int blog) {
+                                            const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
+                                            ull nA, ull n, ull total, ull all_edges, uint32_t* vd, uint32_t* pmin,
+                                            const uint32_t* __restrict__ inv_col, uint32_t hot_words, int C,
+                                            uint64_t W, int blog) {
   constexpr int TILE = 32 * E;
   constexpr int WARPS = THREADS / 32;
   constexpr int SLOT = TILE + 2;
@@ -334,7 +379,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   uint32_t* s_u = s_region + wid * SLOT;
   const uint32_t* s_hot = s_region;
   uint32_t hw = 0;
-  if (!P1 && total >= kHotMinEdges && blog >= 0) hw = hot_words;
+  if (!P1 && all_edges >= kHotMinEdges && blog >= 0) hw = hot_words;
   for (uint32_t k = threadIdx.x; k < (uint32_t)C * hw; k += THREADS) {
     const uint32_t m = k / hw, w = k - m * hw;
     s_region[k] = vd[2 * ((uint64_t)m * W + w)];
@@ -342,8 +387,59 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   __syncthreads();
   const uint32_t hot_bits = hw * 32;
   const uint32_t bmask = (blog >= 0) ? ((1u << blog) - 1u) : 0u;
-  const ull ntiles = (total + TILE - 1) / TILE;
   const ull stride = (ull)gridDim.x * WARPS;
+  // ---- long columns: column-aligned tiles, positions pos + e, no mapping work
+  {
+    const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
+    const int bl = blog > 0 ? blog : 0;
+    constexpr int LWV = E <= 8 ? E : 8;  // all loads of a wave in flight together
+    ull t = (ull)blockIdx.x * WARPS + wid;
+    uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
+    while (t < nA) {
+      const ull nt = t + stride;
+      const uint4 nrec = nt < nA ? tileA[nt] : make_uint4(0, 0, 0, 0);  // prefetch
+      const uint32_t* rp = row + ((ull)rec.x | ((ull)rec.y << 32)) + lane;
+      const uint32_t len = rec.z;
+      uint32_t ug0 = 0;
+      if (P1) ug0 = inv_col[rec.w];
+#pragma unroll
+      for (int wv = 0; wv < E / LWV; ++wv) {
+        uint32_t v[LWV];
+#pragma unroll
+        for (int q = 0; q < LWV; ++q) {
+          v[q] = 0xFFFFFFFFu;
+          ld_stream_u32_if(32u * (LWV * wv + q) + lane < len, rp + 32 * (LWV * wv + q), v[q]);  // Alg.3 line 4
+        }
+        if (P1) {
+          uint32_t ug[LWV];
+#pragma unroll
+          for (int q = 0; q < LWV; ++q) ug[q] = ug0;
+          expand_edges<LWV, true>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+        } else {
+          uint32_t x[LWV], y[LWV];
+#pragma unroll
+          for (int q = 0; q < LWV; ++q) {
+            const bool ok = v[q] != 0xFFFFFFFFu;
+            const uint32_t off = v[q] & bmask;
+            const uint32_t hword = s_hot[ok ? (v[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
+            const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
+            x[q] = 0xFFFFFFFFu;
+            y[q] = 0xFFFFFFFFu;
+            ld_cg_u2_if(ok && !hv, vd + 2 * (v[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
+          }
+#pragma unroll
+          for (int q = 0; q < LWV; ++q) {
+            const uint32_t m = 1u << (v[q] & 31);
+            red_or_if(!((x[q] | y[q]) & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+          }
+        }
+      }
+      t = nt;
+      rec = nrec;
+    }
+  }
+  // ---- short columns: tiles of TILE consecutive short edges, scan + binary-search mapping
+  const ull ntiles = (total + TILE - 1) / TILE;
   // software pipeline: the tile-table entries and the first 32 staged columns of the NEXT tile
   // are loaded while the current tile's row loads and visited tests are in flight.
   ull tile = (ull)blockIdx.x * WARPS + wid;
@@ -401,15 +497,16 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       const uint32_t* rp = row + s_off[0] + lane;
       const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
       const int bl = blog > 0 ? blog : 0;
+      constexpr int LWV = E <= 8 ? E : 8;  // all loads of the wave in flight together
 #pragma unroll
-      for (int wv = 0; wv < E / WV; ++wv) {
-        uint32_t v[WV];
+      for (int wv = 0; wv < E / LWV; ++wv) {
+        uint32_t v[LWV];
 #pragma unroll
-        for (int q = 0; q < WV; ++q) v[q] = ld_stream_u32(rp + 32 * (WV * wv + q));  // Alg.3 line 4
+        for (int q = 0; q < LWV; ++q) v[q] = ld_stream_u32(rp + 32 * (LWV * wv + q));  // Alg.3 line 4
         if (wv == 0) prefetch_next();
-        uint32_t x[WV], y[WV];
+        uint32_t x[LWV], y[LWV];
 #pragma unroll
-        for (int q = 0; q < WV; ++q) {
+        for (int q = 0; q < LWV; ++q) {
           const uint32_t off = v[q] & bmask;
           const uint32_t hword = s_hot[(v[q] >> bl) * hw + (min(off, hclamp) >> 5)];
           const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
@@ -418,7 +515,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ld_cg_u2_if(!hv, vd + 2 * (v[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
         }
 #pragma unroll
-        for (int q = 0; q < WV; ++q) {
+        for (int q = 0; q < LWV; ++q) {
           const uint32_t m = 1u << (v[q] & 31);
           red_or_if(!((x[q] | y[q]) & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
         }
@@ -463,8 +560,18 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         for (int q = 0; q < WV; ++q) {
           const uint32_t e = 32u * (WV * wv + q) + lane;
           const bool ok = e < len;
-          if (__any_sync(0xFFFFFFFFu, ok && e >= cur_end)) {  // some lane crosses a column end
-            while (ok && e >= cur_end) {                      // linear advance
+          {  // linear advance: one step branch-free, more steps (short columns) looped
+            const bool adv = ok && e >= cur_end;
+            idx += adv ? 1u : 0u;
+            const uint32_t nb = s_beg[idx], ne = s_beg[idx + 1];
+            const ull no = s_off[idx];
+            if (adv) {
+              cur_end = ne;
+              base = no - nb;
+            }
+          }
+          if (__any_sync(0xFFFFFFFFu, ok && e >= cur_end)) {  // a lane crossed more than one column
+            while (ok && e >= cur_end) {
               ++idx;
               cur_end = s_beg[idx + 1];
               base = s_off[idx] - s_beg[idx];
@@ -495,17 +602,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
                                                        const ull* __restrict__ rowoff,
                                                        const ull* __restrict__ cumul,
                                                        const uint32_t* __restrict__ tile_k,
+                                                       const uint4* __restrict__ tileA,
                                                        const LevelInfo* __restrict__ info, uint32_t* vd,
                                                        uint32_t* pmin, const uint32_t* __restrict__ inv_col,
                                                        uint32_t hot_words, int C, uint64_t W, int blog) {
-  const ull n = info->n, total = info->edges;
-  if (total == 0) return;
+  const ull n = info->n, total = info->sedges, nA = info->nA, all_edges = info->edges;
+  if (all_edges == 0) return;
   if (info->mode == 1)
-    expand_body<E, THREADS, true>(row, flist, rowoff, cumul, tile_k, n, total, vd, pmin, inv_col, hot_words, C, W,
-                                  blog);
+    expand_body<E, THREADS, true>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+                                  inv_col, hot_words, C, W, blog);
   else
-    expand_body<E, THREADS, false>(row, flist, rowoff, cumul, tile_k, n, total, vd, pmin, inv_col, hot_words, C, W,
-                                   blog);
+    expand_body<E, THREADS, false>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+                                   inv_col, hot_words, C, W, blog);
 }
 
 template <int E, int THREADS>
@@ -532,7 +640,8 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
     cudaFuncSetAttribute(k_expand<E, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
     attr = true;
   }
-  k_expand<E, THREADS><<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.info,
+  k_expand<E, THREADS><<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA,
+                                                        rk.info,
                                                         rk.vd, rk.pmin, rk.inv_col, (uint32_t)hw, g.C,
                                                         g.words_block(), blog);
   return cudaGetLastError();
