@@ -285,7 +285,7 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   G.g.R = R;
   G.g.C = C;
   G.g.block = G.g.npad / P;
-  G.hot_h = G.g.block < (1ull << 20) ? G.g.block : (1ull << 20);
+  G.hot_h = G.g.block < (1ull << 23) ? G.g.block : (1ull << 23);  // degree-ordered prefix
   G.ntuples = nedges;
   CKR(cudaMallocHost(&G.h_scratch, 16 * sizeof(ull)));
   {

@@ -19,6 +19,8 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
+#include <stdlib.h>
+
 #include "kernels.cuh"
 
 namespace bfs200 {
@@ -327,6 +329,7 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 // parent's global id.
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
+constexpr size_t kHotSmem = 96 * 1024;
 
 // One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
 // against the shared-memory copy, the others with one 8-byte load of the visited|discovered
@@ -393,49 +396,81 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
     const int bl = blog > 0 ? blog : 0;
     constexpr int LWV = E <= 8 ? E : 8;  // all loads of a wave in flight together
-    ull t = (ull)blockIdx.x * WARPS + wid;
-    uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
-    while (t < nA) {
-      const ull nt = t + stride;
-      const uint4 nrec = nt < nA ? tileA[nt] : make_uint4(0, 0, 0, 0);  // prefetch
-      const uint32_t* rp = row + ((ull)rec.x | ((ull)rec.y << 32)) + lane;
-      const uint32_t len = rec.z;
-      uint32_t ug0 = 0;
-      if (P1) ug0 = inv_col[rec.w];
+    // Double-buffered: the next tile's row loads are issued before this tile's visited tests,
+    // so each warp keeps two tiles of row data in flight (the level streams `row` from HBM).
+    static_assert(E <= 16, "E");
+    constexpr int LE = E;
+    auto load_rows = [&](const uint4& r, bool valid, uint32_t (&v)[LE]) {
+      const uint32_t* rp = row + ((ull)r.x | ((ull)r.y << 32)) + lane;
+      const uint32_t len = valid ? r.z : 0u;
+#pragma unroll
+      for (int q = 0; q < LE; ++q) {
+        v[q] = 0xFFFFFFFFu;
+        ld_stream_u32_if(32u * q + lane < len, rp + 32 * q, v[q]);  // Alg.3 line 4
+      }
+    };
+    auto process = [&](const uint4& r, const uint32_t (&v)[LE]) {
 #pragma unroll
       for (int wv = 0; wv < E / LWV; ++wv) {
-        uint32_t v[LWV];
+        uint32_t vw[LWV];
 #pragma unroll
-        for (int q = 0; q < LWV; ++q) {
-          v[q] = 0xFFFFFFFFu;
-          ld_stream_u32_if(32u * (LWV * wv + q) + lane < len, rp + 32 * (LWV * wv + q), v[q]);  // Alg.3 line 4
-        }
+        for (int q = 0; q < LWV; ++q) vw[q] = v[LWV * wv + q];
         if (P1) {
           uint32_t ug[LWV];
+          const uint32_t ug0 = inv_col[r.w];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
-          expand_edges<LWV, true>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+          expand_edges<LWV, true>(vw, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
         } else {
           uint32_t x[LWV], y[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) {
-            const bool ok = v[q] != 0xFFFFFFFFu;
-            const uint32_t off = v[q] & bmask;
-            const uint32_t hword = s_hot[ok ? (v[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
+            const bool ok = vw[q] != 0xFFFFFFFFu;
+            const uint32_t off = vw[q] & bmask;
+            const uint32_t hword = s_hot[ok ? (vw[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
             const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
             x[q] = 0xFFFFFFFFu;
             y[q] = 0xFFFFFFFFu;
-            ld_cg_u2_if(ok && !hv, vd + 2 * (v[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
+            ld_cg_u2_if(ok && !hv, vd + 2 * (vw[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
           }
 #pragma unroll
           for (int q = 0; q < LWV; ++q) {
-            const uint32_t m = 1u << (v[q] & 31);
-            red_or_if(!((x[q] | y[q]) & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+            const uint32_t m = 1u << (vw[q] & 31);
+            red_or_if(!((x[q] | y[q]) & m), vd + 2 * (vw[q] >> 5) + 1, m);  // Alg.3 line 7
           }
         }
       }
-      t = nt;
-      rec = nrec;
+    };
+    ull t = (ull)blockIdx.x * WARPS + wid;
+    uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
+    ull t1 = t + stride;
+    uint4 rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
+    if (E <= 8) {
+      uint32_t v[LE];
+      load_rows(rec, t < nA, v);
+      while (t < nA) {
+        const ull t2 = t1 + stride;
+        const uint4 rec2 = t2 < nA ? tileA[t2] : make_uint4(0, 0, 0, 0);
+        uint32_t vn[LE];
+        load_rows(rec1, t1 < nA, vn);
+        process(rec, v);
+#pragma unroll
+        for (int q = 0; q < LE; ++q) v[q] = vn[q];
+        rec = rec1;
+        rec1 = rec2;
+        t = t1;
+        t1 = t2;
+      }
+    } else {
+      while (t < nA) {
+        uint32_t v[LE];
+        load_rows(rec, true, v);
+        process(rec, v);
+        rec = rec1;
+        t = t1;
+        t1 = t + stride;
+        rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
+      }
     }
   }
   // ---- short columns: tiles of TILE consecutive short edges, scan + binary-search mapping
@@ -629,7 +664,14 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
     while ((1ull << blog) < g.block) ++blog;
   }
   uint64_t hw = hot_h / 32;
-  const uint64_t cap = (kSmemBudget - staging - 16) / 4 / (uint64_t)g.C;
+  // the hot copy gets at most kHotSmem bytes: the rest of the SM's 228 KB stays L1 cache
+  static size_t hot_smem = 0;
+  if (!hot_smem) {  // tuning knob for experiments: BFS200_HOT_KB (default 128)
+    const char* env = getenv("BFS200_HOT_KB");
+    hot_smem = (env && atoi(env) > 0) ? (size_t)atoi(env) * 1024 : kHotSmem;
+  }
+  const uint64_t budget = hot_smem < kSmemBudget - staging - 16 ? hot_smem : kSmemBudget - staging - 16;
+  const uint64_t cap = budget / 4 / (uint64_t)g.C;
   if (hw > cap) hw = cap;
   if (blog < 0) hw = 0;
   size_t region = (size_t)g.C * hw * 4;
