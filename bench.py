@@ -227,7 +227,8 @@ def run_ours(args, rank, world, local_rank):
 
     times, mcomps, launches = [], [], 0
     exp_bytes, exp_ms, lvl_tot = 0.0, 0.0, 0
-    phase = {"expand_comm": 0.0, "scan": 0.0, "expand": 0.0, "fold_comm": 0.0, "update": 0.0, "allreduce": 0.0}
+    phase = {"expand_comm": 0.0, "scan": 0.0, "expand": 0.0, "parent": 0.0, "fold_comm": 0.0, "update": 0.0,
+             "allreduce": 0.0}
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             r = timed_roots[k % len(timed_roots)]

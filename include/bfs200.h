@@ -100,6 +100,7 @@ typedef struct {
   double expand_comm; /* column all-gather of the frontier bitmap        */
   double scan;        /* frontier unpack + degree exclusive scan    */
   double expand;      /* frontier expansion kernel                         (Alg.3)        */
+  double parent;      /* parent claim of the rows discovered in the level  (Alg.3 l.17)   */
   double fold_comm;   /* row exchange of discovered-vertex bitmaps        */
   double update;      /* frontier update + pack    */
   double allreduce;   /* termination reduction + host read        */

@@ -50,7 +50,7 @@ class Stats(ctypes.Structure):
 
 class LevelRecord(ctypes.Structure):
     _fields_ = [("expand_comm", ctypes.c_double), ("scan", ctypes.c_double), ("expand", ctypes.c_double),
-                ("fold_comm", ctypes.c_double), ("update", ctypes.c_double), ("allreduce", ctypes.c_double),
+                ("parent", ctypes.c_double), ("fold_comm", ctypes.c_double), ("update", ctypes.c_double), ("allreduce", ctypes.c_double),
                 ("frontier", ctypes.c_uint64), ("edges", ctypes.c_uint64)]
 
 

@@ -17,6 +17,7 @@ constexpr int kScanSegWords = 256;         // bitmap words per warp segment of t
 constexpr int kScanThreads = 256;          // 8 warps = 8 segments per CTA
 constexpr int kExpandThreads = 256;
 constexpr int kMaxLevels = 4096;
+constexpr int kPhaseEvents = 8;  // event boundaries per level (bfs_level_record phases + 1)
 
 // Device-side per-level counters written by the scan kernels (read by the expansion kernel,
 // so the host never needs the frontier size to launch it).
@@ -31,7 +32,8 @@ struct LevelInfo {
   unsigned long long nA;      // long-column tiles (tileA records)
   unsigned long long ncols;   // short columns (stats)
   unsigned long long nlongcols;  // long columns (stats)
-  unsigned long long pad[7];
+  unsigned long long disc_total;  // rows discovered by this rank so far in this search (K4 counts)
+  unsigned long long pad[6];
 };
 
 // Geometry of the 2D partition (index maps SPEC.md S:109-148).
@@ -47,6 +49,7 @@ struct Geom {
 struct Rank {
   int r, i, j;        // r = j*R + i
   uint64_t nnz = 0;   // CSC entries
+  uint64_t nz_rows = 0;  // local rows with at least one entry (for the parent-mode heuristic)
   unsigned long long* col = nullptr;  // [ncols+1] column offsets (u64: nnz can exceed 2^32)
   uint32_t* row = nullptr;    // [nnz] local row ids, ascending within each column
   // CSR view of the same local matrix (row -> ascending local columns) for the parent pass;

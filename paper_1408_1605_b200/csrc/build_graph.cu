@@ -329,6 +329,16 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   return BFS_OK;
 }
 
+// rows with at least one entry (csr_ptr[r+1] > csr_ptr[r]) -> *out
+__global__ void k_count_nz_rows(const ull* ptr, uint64_t nrows, ull* out) {
+  unsigned c = 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (uint64_t)gridDim.x * blockDim.x)
+    c += ptr[r + 1] > ptr[r] ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (ull)c);
+}
+
 // per-rank slices of the permutation: fwd_own / inv_own (local offsets of the owned block) and
 // inv_col (relabeled local column -> ORIGINAL global id, the value stored as parent)
 static int rank_maps(Graph& G, Rank& rk, const uint32_t* fwd, const uint32_t* inv) {
@@ -338,6 +348,17 @@ static int rank_maps(Graph& G, Rank& rk, const uint32_t* fwd, const uint32_t* in
   if ((rc = G_alloc(G, (void**)&rk.fwd_own, g.block * 4))) return rc;
   if ((rc = G_alloc(G, (void**)&rk.inv_own, g.block * 4))) return rc;
   if ((rc = G_alloc(G, (void**)&rk.inv_col, g.ncols() * 4))) return rc;
+  {
+    ull* cnt = nullptr;
+    ull h = 0;
+    CKR(cudaMalloc(&cnt, sizeof(ull)));
+    CKR(cudaMemsetAsync(cnt, 0, sizeof(ull), s));
+    k_count_nz_rows<<<1024, 256, 0, s>>>(rk.csr_ptr, g.nrows(), cnt);
+    CKR(cudaMemcpyAsync(&h, cnt, sizeof(ull), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+    cudaFree(cnt);
+    rk.nz_rows = h;
+  }
   const uint64_t vb = (uint64_t)rk.r * g.block;
   k_slice<<<1024, 256, 0, s>>>(fwd, vb, g.block, (uint32_t)vb, rk.fwd_own);
   k_slice<<<1024, 256, 0, s>>>(inv, vb, g.block, (uint32_t)vb, rk.inv_own);

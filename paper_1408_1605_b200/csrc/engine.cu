@@ -324,7 +324,7 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
 
 // ------------------------------------------------------------------ phase events
 static int ev_prepare(Graph& G, int level) {
-  const size_t need = (size_t)(level + 1) * 7;
+  const size_t need = (size_t)(level + 1) * kPhaseEvents;
   while (G.ev.size() < need) {
     cudaEvent_t e;
     CKR(cudaEventCreate(&e));
@@ -337,7 +337,7 @@ static inline int ev_rec(Graph& G, int level, int p) {
   if (!G.opts.phase_timing) return BFS_OK;
   int rc = ev_prepare(G, level);
   if (rc) return rc;
-  CKR(cudaEventRecord(G.ev[(size_t)level * 7 + p], G.stream));
+  CKR(cudaEventRecord(G.ev[(size_t)level * kPhaseEvents + p], G.stream));
   return BFS_OK;
 }
 
@@ -434,15 +434,16 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
     if ((rc = ev_rec(G, nlev, 2))) return rc;
     for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, s));
-    for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
     if ((rc = ev_rec(G, nlev, 3))) return rc;
-    if ((rc = fold_exchange(G))) return rc;
+    for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
     if ((rc = ev_rec(G, nlev, 4))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_update(g, rk, lvl, s));
+    if ((rc = fold_exchange(G))) return rc;
     if ((rc = ev_rec(G, nlev, 5))) return rc;
+    for (Rank& rk : G.ranks) CKR(launch_update(g, rk, lvl, s));
+    if ((rc = ev_rec(G, nlev, 6))) return rc;
     if (G.world_size > 1) NKR(ncclAllReduce(&G.infos[0].newv, &G.infos[0].newv, 1, ncclUint64, ncclSum, G.world, s));
     CKR(cudaMemcpyAsync(G.h_infos, G.infos, G.ranks.size() * sizeof(LevelInfo), cudaMemcpyDeviceToHost, s));
-    if ((rc = ev_rec(G, nlev, 6))) return rc;
+    if ((rc = ev_rec(G, nlev, 7))) return rc;
     CKR(cudaStreamSynchronize(s));
     ull total_new = 0, fr = 0, ed = 0;
     for (size_t k = 0; k < G.ranks.size(); ++k) {
@@ -645,17 +646,18 @@ int bfs_level_times(bfs_graph* gp, bfs_level_record* out, int max_levels, int* n
   const int n = G.last_levels < max_levels ? G.last_levels : max_levels;
   if (n > 0 && !out) return set_err(BFS_EINVAL, "null output");
   for (int l = 0; l < n; ++l) {
-    float t[6];
-    for (int p = 0; p < 6; ++p) {
-      CKR(cudaEventSynchronize(G.ev[(size_t)l * 7 + p + 1]));
-      CKR(cudaEventElapsedTime(&t[p], G.ev[(size_t)l * 7 + p], G.ev[(size_t)l * 7 + p + 1]));
+    float t[kPhaseEvents - 1];
+    for (int p = 0; p < kPhaseEvents - 1; ++p) {
+      CKR(cudaEventSynchronize(G.ev[(size_t)l * kPhaseEvents + p + 1]));
+      CKR(cudaEventElapsedTime(&t[p], G.ev[(size_t)l * kPhaseEvents + p], G.ev[(size_t)l * kPhaseEvents + p + 1]));
     }
     out[l].expand_comm = t[0];
     out[l].scan = t[1];
     out[l].expand = t[2];
-    out[l].fold_comm = t[3];
-    out[l].update = t[4];
-    out[l].allreduce = t[5];
+    out[l].parent = t[3];
+    out[l].fold_comm = t[4];
+    out[l].update = t[5];
+    out[l].allreduce = t[6];
     out[l].frontier = G.lvl_frontier[l];
     out[l].edges = G.lvl_edges[l];
   }

@@ -95,6 +95,7 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
   const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
   cudaMemsetAsync(rk.vd, 0, 2 * rw * 4, s);
   cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
+  cudaMemsetAsync(&rk.info->disc_total, 0, sizeof(ull), s);
   if (owner) {
     const uint64_t t = root - (uint64_t)rk.r * g.block;
     k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
 
 // exclusive scan over segments (one CTA); writes the level totals, cumul[n]; resets counters
 __global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const SegTot* seg_tot, SegTot* seg_off,
-                                                    LevelInfo* info, ull* cumul, ull nnz) {
+                                                    LevelInfo* info, ull* cumul, ull nnz, ull p2_factor,
+                                                    ull nz_rows) {
   typedef cub::BlockScan<SegTot, 1024> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ SegTot carry;
@@ -195,9 +197,13 @@ __global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const SegTot*
     info->newv = 0;
     // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
     // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-    // the scan (P2) is used when that is <= 4; otherwise (small frontiers, e.g. the first
-    // levels) the expansion does compare-then-atomicMin per candidate edge (P1).
-    info->mode = ((c.ss + c.ls) * 4ull >= nnz) ? 2ull : 1ull;
+    // the scan (P2) is used when that is <= p2_factor (default 4); otherwise (small frontiers,
+    // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).
+    // P2 also when few rows remain to be discovered (the scans are then few, whatever their length):
+    // remaining = rows with entries - rows discovered so far (an estimate on this rank).
+    const ull edges = c.ss + c.ls, seen = info->disc_total;
+    const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
+    info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
     info->nlong = 0;
     info->nlongcols = 0;
     cumul[c.cs] = c.ss;
@@ -308,7 +314,12 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   SegTot* st = static_cast<SegTot*>(rk.seg_tot);
   SegTot* so = static_cast<SegTot*>(rk.seg_off);
   k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
-  k_scan_segs<<<1, 1024, 0, s>>>(nseg, st, so, rk.info, rk.cumul, (ull)rk.nnz);
+  static ull p2_factor = 0;
+  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 4)
+    const char* env = getenv("BFS200_P2_FACTOR");
+    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 4ull;
+  }
+  k_scan_segs<<<1, 1024, 0, s>>>(nseg, st, so, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
@@ -409,7 +420,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         ld_stream_u32_if(32u * q + lane < len, rp + 32 * q, v[q]);  // Alg.3 line 4
       }
     };
-    auto process = [&](const uint4& r, const uint32_t (&v)[LE]) {
+    auto process = [&](const uint4& r, const uint32_t (&v)[LE], uint32_t ug0) {
 #pragma unroll
       for (int wv = 0; wv < E / LWV; ++wv) {
         uint32_t vw[LWV];
@@ -417,7 +428,6 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         for (int q = 0; q < LWV; ++q) vw[q] = v[LWV * wv + q];
         if (P1) {
           uint32_t ug[LWV];
-          const uint32_t ug0 = inv_col[r.w];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
           expand_edges<LWV, true>(vw, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
@@ -445,17 +455,22 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;
     uint4 rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
+    // P1: the parent's original id of the tile's column (prefetched with the rows)
+    auto col_id = [&](const uint4& r, bool valid) -> uint32_t { return (P1 && valid) ? inv_col[r.w] : 0u; };
     if (E <= 8) {
       uint32_t v[LE];
       load_rows(rec, t < nA, v);
+      uint32_t ug = col_id(rec, t < nA);
       while (t < nA) {
         const ull t2 = t1 + stride;
         const uint4 rec2 = t2 < nA ? tileA[t2] : make_uint4(0, 0, 0, 0);
         uint32_t vn[LE];
         load_rows(rec1, t1 < nA, vn);
-        process(rec, v);
+        const uint32_t ugn = col_id(rec1, t1 < nA);
+        process(rec, v, ug);
 #pragma unroll
         for (int q = 0; q < LE; ++q) v[q] = vn[q];
+        ug = ugn;
         rec = rec1;
         rec1 = rec2;
         t = t1;
@@ -465,7 +480,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       while (t < nA) {
         uint32_t v[LE];
         load_rows(rec, true, v);
-        process(rec, v);
+        process(rec, v, col_id(rec, true));
         rec = rec1;
         t = t1;
         t1 = t + stride;
@@ -720,16 +735,18 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
                                                             const uint32_t* __restrict__ front, uint32_t* pred,
                                                             uint32_t* pmin, uint32_t* sendbuf,
                                                             const uint32_t* __restrict__ inv_col,
-                                                            const LevelInfo* __restrict__ info) {
+                                                            LevelInfo* info) {
   __shared__ uint32_t queue[kParentThreads / 32][1024];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool p1 = info->mode == 1;
+  unsigned ndisc = 0;
   const uint64_t nchunks = (nwords + 31) / 32;
   for (uint64_t ch = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid; ch < nchunks;
        ch += (uint64_t)gridDim.x * (kParentThreads / 32)) {
     const uint64_t w = ch * 32 + lane;
     const uint32_t d = (w < nwords) ? vd[2 * w + 1] : 0u;
     if (sendbuf && w < nwords) sendbuf[w] = d;
+    ndisc += __popc(d);
     if (!__any_sync(0xFFFFFFFFu, d != 0)) continue;
     if (p1) {
       uint32_t b = d;
@@ -812,6 +829,9 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
     }
     __syncwarp();
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ndisc += __shfl_xor_sync(0xFFFFFFFFu, ndisc, o);
+  if (lane == 0 && ndisc) atomicAdd(&info->disc_total, (ull)ndisc);
 }
 
 cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
