@@ -80,7 +80,9 @@ struct Rank {
   uint32_t* tile_k = nullptr;            // [nnz/32 + 2] first frontier index of every expansion tile
   uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
   void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
-  void* seg_off = nullptr;               // [nseg] their exclusive scan
+  void* seg_off = nullptr;               // [nseg+1] their exclusive scan (seg_off[nseg] = level total)
+  void* seg_tmp = nullptr;               // CUB temp of the segment scan
+  size_t seg_tmp_bytes = 0;
   uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution

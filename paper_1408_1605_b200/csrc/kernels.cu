@@ -121,6 +121,7 @@ struct SegTot {
   ull ss;           // short edges
   ull ls;           // long edges
 };
+static_assert(sizeof(SegTot) == 24, "engine.cu allocates 24 B per segment");
 struct SegAdd {
   __device__ __forceinline__ SegTot operator()(const SegTot& a, const SegTot& b) const {
     return SegTot{a.cs + b.cs, a.na + b.na, a.ss + b.ss, a.ls + b.ls};
@@ -140,13 +141,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   for (uint64_t wb = w0; wb < w1; wb += 32) {
     const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
     unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
-    while (nz) {
-      const int jw = __ffs(nz) - 1;
-      nz &= nz - 1;
-      const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
-      if ((xw >> lane) & 1u) {
-        const uint64_t u = (wb + jw) * 32 + lane;
-        const ull d = __ldg(col + u + 1) - __ldg(col + u);
+    while (nz) {  // 4 non-zero words at a time: their col[] loads are in flight together
+      ull c0[4], c1[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int jw = nz ? __ffs(nz) - 1 : -1;
+        nz &= nz ? nz - 1 : 0u;
+        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
+        const bool bit = jw >= 0 && ((xw >> lane) & 1u);
+        const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
+        c0[b] = bit ? __ldg(col + u) : 0ull;
+        c1[b] = bit ? __ldg(col + u + 1) : 0ull;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const ull d = c1[b] - c0[b];
         if (d >= half) {
           t.na += (unsigned)((d + tm) >> tile_shift);
           t.ls += d;
@@ -167,47 +176,35 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   if (lane == 0) seg_tot[seg] = t;
 }
 
-// exclusive scan over segments (one CTA); writes the level totals, cumul[n]; resets counters
-__global__ void __launch_bounds__(1024) k_scan_segs(uint64_t nseg, const SegTot* seg_tot, SegTot* seg_off,
-                                                    LevelInfo* info, ull* cumul, ull nnz, ull p2_factor,
-                                                    ull nz_rows) {
-  typedef cub::BlockScan<SegTot, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ SegTot carry;
-  if (threadIdx.x == 0) carry = SegTot{0u, 0u, 0ull, 0ull};
-  __syncthreads();
-  for (uint64_t base = 0; base < nseg; base += 1024) {
-    const uint64_t t = base + threadIdx.x;
-    SegTot v = (t < nseg) ? seg_tot[t] : SegTot{0u, 0u, 0ull, 0ull};
-    SegTot ex, agg;
-    BS(tmp).ExclusiveScan(v, ex, SegTot{0u, 0u, 0ull, 0ull}, SegAdd(), agg);
-    const SegTot c0 = carry;
-    if (t < nseg) seg_off[t] = SegAdd()(c0, ex);
-    __syncthreads();
-    if (threadIdx.x == 0) carry = SegAdd()(c0, agg);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const SegTot c = carry;
-    info->n = c.cs;
-    info->sedges = c.ss;
-    info->nA = c.na;
-    info->edges = c.ss + c.ls;
-    info->ncols = c.cs + 0ull;  // long columns are counted by k_scan_emit (info->nlongcols)
-    info->newv = 0;
-    // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
-    // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-    // the scan (P2) is used when that is <= p2_factor (default 4); otherwise (small frontiers,
-    // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).
-    // P2 also when few rows remain to be discovered (the scans are then few, whatever their length):
-    // remaining = rows with entries - rows discovered so far (an estimate on this rank).
-    const ull edges = c.ss + c.ls, seen = info->disc_total;
-    const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
-    info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
-    info->nlong = 0;
-    info->nlongcols = 0;
-    cumul[c.cs] = c.ss;
-  }
+// level totals from the segment scan (seg_off[nseg] = sum over all segments); resets counters
+__global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* info, ull* cumul, ull nnz,
+                             ull p2_factor, ull nz_rows) {
+  const SegTot c = seg_off[nseg];
+  info->n = c.cs;
+  info->sedges = c.ss;
+  info->nA = c.na;
+  info->edges = c.ss + c.ls;
+  info->ncols = c.cs;
+  info->newv = 0;
+  // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
+  // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
+  // the scan (P2) is used when that is <= p2_factor (default 4); otherwise (small frontiers,
+  // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).  P2 also when
+  // few rows remain to be discovered (the scans are then few, whatever their length):
+  // remaining = rows with entries - rows discovered so far (an estimate on this rank).
+  const ull edges = c.ss + c.ls, seen = info->disc_total;
+  const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
+  info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
+  info->nlong = 0;
+  info->nlongcols = 0;
+  cumul[c.cs] = c.ss;
+}
+
+size_t seg_scan_tmp_bytes(uint64_t nseg) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const SegTot*)nullptr, (SegTot*)nullptr, SegAdd(),
+                                 SegTot{0u, 0u, 0ull, 0ull}, (uint64_t)nseg + 1);
+  return bytes;
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
@@ -230,58 +227,68 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   for (uint64_t wb = w0; wb < w1; wb += 32) {
     const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
     unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
-    while (nz) {
-      const int jw = __ffs(nz) - 1;
-      nz &= nz - 1;
-      const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
-      const uint64_t u = (wb + jw) * 32 + lane;
-      ull c0 = 0, d = 0;
-      if ((xw >> lane) & 1u) {
-        c0 = __ldg(col + u);
-        d = __ldg(col + u + 1) - c0;
-      }
-      const bool isl = d >= half;
-      const ull ds = isl ? 0ull : d;
-      const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
-      const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
-      ull inc = ds;     // inclusive warp scan of short degrees
-      unsigned ia = na; // inclusive warp scan of long-tile counts
+    while (nz) {  // 4 non-zero words at a time: their col[] loads are in flight together
+      int jwb[4];
+      ull c0b[4], c1b[4];
 #pragma unroll
-      for (int s2 = 1; s2 < 32; s2 <<= 1) {
-        const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
-        const unsigned ya = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
-        if (lane >= s2) {
-          inc += y;
-          ia += ya;
-        }
+      for (int b = 0; b < 4; ++b) {
+        const int jw = nz ? __ffs(nz) - 1 : -1;
+        nz &= nz ? nz - 1 : 0u;
+        jwb[b] = jw;
+        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
+        const bool bit = jw >= 0 && ((xw >> lane) & 1u);
+        const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
+        c0b[b] = bit ? __ldg(col + u) : 0ull;
+        c1b[b] = bit ? __ldg(col + u + 1) : 0ull;
       }
-      if (ds) {
-        const uint64_t pos = k + __popc(smask & lt);
-        const ull eb = e + inc - ds;
-        flist[pos] = (uint32_t)u;
-        rowoff[pos] = c0;
-        cumul[pos] = eb;
-        // a short column spans at most two tiles
-        for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
-      }
-      if (isl) {
-        const uint64_t pa = a + ia - na;
-        if (na <= 8) {
-          for (unsigned q = 0; q < na; ++q) {
-            const ull pos = c0 + ((ull)q << tile_shift);
-            const ull len = min(d - ((ull)q << tile_shift), tm + 1);
-            tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (jwb[b] < 0) break;  // warp-uniform
+        const uint64_t u = (wb + jwb[b]) * 32 + lane;
+        const ull c0 = c0b[b], d = c1b[b] - c0b[b];
+        const bool isl = d >= half;
+        const ull ds = isl ? 0ull : d;
+        const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
+        const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
+        ull inc = ds;     // inclusive warp scan of short degrees
+        unsigned ia = na; // inclusive warp scan of long-tile counts
+#pragma unroll
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+          const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
+          const unsigned ya = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
+          if (lane >= s2) {
+            inc += y;
+            ia += ya;
           }
-        } else {  // hub column: its tiles are written by k_tile_fill
-          const ull slot = atomicAdd(&info->nlong, 1ull);
-          longlist[2 * slot] = make_uint4((uint32_t)pa, na, (uint32_t)u, (uint32_t)(pa >> 32));
-          longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
         }
-        ++nlongcols;
+        if (ds) {
+          const uint64_t pos = k + __popc(smask & lt);
+          const ull eb = e + inc - ds;
+          flist[pos] = (uint32_t)u;
+          rowoff[pos] = c0;
+          cumul[pos] = eb;
+          // a short column spans at most two tiles
+          for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
+        }
+        if (isl) {
+          const uint64_t pa = a + ia - na;
+          if (na <= 8) {
+            for (unsigned q = 0; q < na; ++q) {
+              const ull pos = c0 + ((ull)q << tile_shift);
+              const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+              tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
+            }
+          } else {  // hub column: its tiles are written by k_tile_fill
+            const ull slot = atomicAdd(&info->nlong, 1ull);
+            longlist[2 * slot] = make_uint4((uint32_t)pa, na, (uint32_t)u, (uint32_t)(pa >> 32));
+            longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
+          }
+          ++nlongcols;
+        }
+        k += __popc(smask);
+        e += __shfl_sync(0xFFFFFFFFu, inc, 31);
+        a += __shfl_sync(0xFFFFFFFFu, ia, 31);
       }
-      k += __popc(smask);
-      e += __shfl_sync(0xFFFFFFFFu, inc, 31);
-      a += __shfl_sync(0xFFFFFFFFu, ia, 31);
     }
   }
 #pragma unroll
@@ -314,12 +321,15 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   SegTot* st = static_cast<SegTot*>(rk.seg_tot);
   SegTot* so = static_cast<SegTot*>(rk.seg_off);
   k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
+  // exclusive scan over nseg+1 segment totals (st[nseg] stays zero) -> so[nseg] = level total
+  cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0ull, 0ull},
+                                 (uint64_t)nseg + 1, s);
   static ull p2_factor = 0;
   if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 4)
     const char* env = getenv("BFS200_P2_FACTOR");
     p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 4ull;
   }
-  k_scan_segs<<<1, 1024, 0, s>>>(nseg, st, so, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
+  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
