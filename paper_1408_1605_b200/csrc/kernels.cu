@@ -736,20 +736,39 @@ cudaError_t launch_expand(const Geom& g, Rank& rk, int E, uint64_t hot_h, cudaSt
 //     hit by then are finished by the whole warp, 32 entries per step (ballot -> first lane).
 // A warp takes 32 consecutive words and queues their rows in shared memory.  With C > 1 the
 // discovered words are also packed contiguously as the fold message.
-constexpr int kParentThreads = 256;
+constexpr int kParentThreads = 1024;
 constexpr int kShortScan = 32;
+constexpr size_t kParentHotSmem = 64 * 1024;  // hot prefix of the frontier bitmap (P2 levels)
 
-__global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __restrict__ vd, uint64_t nwords,
-                                                            const ull* __restrict__ csr_ptr,
-                                                            const uint32_t* __restrict__ csr_col,
-                                                            const uint32_t* __restrict__ front, uint32_t* pred,
-                                                            uint32_t* pmin, uint32_t* sendbuf,
-                                                            const uint32_t* __restrict__ inv_col,
-                                                            LevelInfo* info) {
-  __shared__ uint32_t queue[kParentThreads / 32][1024];
+__global__ void __launch_bounds__(kParentThreads, 1) k_parent(const uint32_t* __restrict__ vd, uint64_t nwords,
+                                                               const ull* __restrict__ csr_ptr,
+                                                               const uint32_t* __restrict__ csr_col,
+                                                               const uint32_t* __restrict__ front, uint32_t* pred,
+                                                               uint32_t* pmin, uint32_t* sendbuf,
+                                                               const uint32_t* __restrict__ inv_col,
+                                                               LevelInfo* info, uint32_t hot_words, int R,
+                                                               uint64_t Wc, int blog) {
+  extern __shared__ __align__(16) unsigned char psmem[];
+  uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
+  uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool p1 = info->mode == 1;
   unsigned ndisc = 0;
+  // P2: frontier bits of the hot (relabeled, highest-degree) column prefix of each of the R
+  // column segments, so most frontier tests of the CSR scans stay in shared memory
+  const uint32_t hw = (!p1 && blog >= 0) ? hot_words : 0u;
+  for (uint32_t k = threadIdx.x; k < (uint32_t)R * hw; k += kParentThreads) {
+    const uint32_t m = k / hw, w = k - m * hw;
+    s_hot[k] = front[(uint64_t)m * Wc + w];
+  }
+  __syncthreads();
+  const uint32_t hot_bits = hw * 32, bmask = (blog >= 0) ? ((1u << blog) - 1u) : 0u;
+  const int bl = blog > 0 ? blog : 0;
+  auto in_front = [&](uint32_t u) -> bool {
+    const uint32_t off = u & bmask;
+    if (off < hot_bits) return (s_hot[(u >> bl) * hw + (off >> 5)] >> (off & 31)) & 1u;
+    return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
+  };
   const uint64_t nchunks = (nwords + 31) / 32;
   for (uint64_t ch = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid; ch < nchunks;
        ch += (uint64_t)gridDim.x * (kParentThreads / 32)) {
@@ -800,7 +819,7 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
         for (int k = 0; k < 4; ++k) u[k] = (p + k < stop) ? __ldg(csr_col + p + k) : 0xFFFFFFFFu;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          f[k] = (u[k] != 0xFFFFFFFFu) && ((__ldg(front + (u[k] >> 5)) >> (u[k] & 31)) & 1u);
+          f[k] = (u[k] != 0xFFFFFFFFu) && in_front(u[k]);
 #pragma unroll
         for (int k = 3; k >= 0; --k)
           if (f[k]) best = u[k];
@@ -827,7 +846,7 @@ __global__ void __launch_bounds__(kParentThreads) k_parent(const uint32_t* __res
         uint32_t best = 0xFFFFFFFFu;
         for (ull p = csr_ptr[r] + kShortScan; p < end; p += 32) {
           const uint32_t u = (p + lane < end) ? __ldg(csr_col + p + lane) : 0xFFFFFFFFu;
-          const bool f = (u != 0xFFFFFFFFu) && ((__ldg(front + (u >> 5)) >> (u & 31)) & 1u);
+          const bool f = (u != 0xFFFFFFFFu) && in_front(u);
           const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
           if (m) {
             best = __shfl_sync(0xFFFFFFFFu, u, __ffs(m) - 1);
@@ -848,10 +867,25 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t nwords = g.nrows() / 32;
   const uint64_t nchunks = (nwords + 31) / 32;
   uint64_t grid = (nchunks + kParentThreads / 32 - 1) / (kParentThreads / 32);
-  const uint64_t cap = (uint64_t)num_sms() * 4;
+  const uint64_t cap = (uint64_t)num_sms();
   if (grid > cap) grid = cap;
-  k_parent<<<(unsigned)grid, kParentThreads, 0, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
-                                                     rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info);
+  int blog = -1;
+  if (g.block && (g.block & (g.block - 1)) == 0) {
+    blog = 0;
+    while ((1ull << blog) < g.block) ++blog;
+  }
+  uint64_t hw = kParentHotSmem / 4 / (uint64_t)g.R;
+  if (hw > g.words_block()) hw = g.words_block();
+  if (blog < 0) hw = 0;
+  const size_t smem = (size_t)(kParentThreads / 32) * 1024 * 4 + (size_t)(g.R * hw > 4 ? g.R * hw : 4) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    attr = true;
+  }
+  k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
+                                                        rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
+                                                        (uint32_t)hw, g.R, g.words_block(), blog);
   return cudaGetLastError();
 }
 
