@@ -383,7 +383,7 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
   }
 }
 
-template <int E, int THREADS, bool P1>
+template <int E, int THREADS, bool P1, bool SEG1>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
                                             const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
@@ -446,9 +446,15 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
 #pragma unroll
           for (int q = 0; q < LWV; ++q) {
             const bool ok = vw[q] != 0xFFFFFFFFu;
-            const uint32_t off = vw[q] & bmask;
-            const uint32_t hword = s_hot[ok ? (vw[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
-            const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
+            bool hv;
+            if (SEG1) {  // one row segment (C == 1): the row id is the offset; invalid ids are not hot
+              const uint32_t hword = s_hot[min(vw[q], hclamp) >> 5];
+              hv = vw[q] < hot_bits && ((hword >> (vw[q] & 31)) & 1u);
+            } else {
+              const uint32_t off = vw[q] & bmask;
+              const uint32_t hword = s_hot[ok ? (vw[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
+              hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
+            }
             x[q] = 0xFFFFFFFFu;
             y[q] = 0xFFFFFFFFu;
             ld_cg_u2_if(ok && !hv, vd + 2 * (vw[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
@@ -656,7 +662,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   }
 }
 
-template <int E, int THREADS>
+template <int E, int THREADS, bool SEG1>
 __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
                                                        const uint32_t* __restrict__ flist,
                                                        const ull* __restrict__ rowoff,
@@ -669,10 +675,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
   const ull n = info->n, total = info->sedges, nA = info->nA, all_edges = info->edges;
   if (all_edges == 0) return;
   if (info->mode == 1)
-    expand_body<E, THREADS, true>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+    expand_body<E, THREADS, true, SEG1>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
                                   inv_col, hot_words, C, W, blog);
   else
-    expand_body<E, THREADS, false>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+    expand_body<E, THREADS, false, SEG1>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
                                    inv_col, hot_words, C, W, blog);
 }
 
@@ -704,10 +710,12 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   const size_t smem = staging + region + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_expand<E, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
     attr = true;
   }
-  k_expand<E, THREADS><<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA,
+  auto kern = g.C == 1 ? k_expand<E, THREADS, true> : k_expand<E, THREADS, false>;
+  kern<<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA,
                                                         rk.info,
                                                         rk.vd, rk.pmin, rk.inv_col, (uint32_t)hw, g.C,
                                                         g.words_block(), blog);
@@ -950,13 +958,14 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
 // For owned t: unreached (visited bit clear) -> level -1, parent -1; reached with the winner
 // column == own column (always when C == 1) -> parent = pred of the own row segment; other
 // reached vertices are filled by the resolution exchange (k_resp_scatter).
-// t indexes the ORIGINAL owned offsets (outputs); p = fwd_own[t] the relabeled one (state).
+// p indexes the relabeled owned offsets (state, read coalesced); t = inv_own[p] the ORIGINAL one
+// (outputs; identity outside the relabeled prefix, so most writes are coalesced too).
 __global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const uint32_t* pred_own,
-                           const uint8_t* winner, const uint32_t* fwd_own, int j, uint64_t block, int64_t* parent_out,
+                           const uint8_t* winner, const uint32_t* inv_own, int j, uint64_t block, int64_t* parent_out,
                            int32_t* level_out) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= block) return;
-  const uint32_t p = fwd_own[t];
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= block) return;
+  const uint32_t t = inv_own[p];
   const bool reached = (vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
   if (parent_out) {
     int64_t q = -1;
@@ -969,7 +978,7 @@ __global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const u
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
   const unsigned grid = (unsigned)((g.block + 255) / 256);
   k_finalize<<<grid, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.level,
-                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.fwd_own, rk.j,
+                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.inv_own, rk.j,
                                   g.block, parent_out, level_out);
   return cudaGetLastError();
 }
