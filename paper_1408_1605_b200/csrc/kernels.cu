@@ -128,6 +128,8 @@ struct SegAdd {
   }
 };
 
+// Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
+// chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                               uint64_t nseg, const ull* __restrict__ col,
                                                               SegTot* seg_tot, int tile_shift) {
@@ -138,24 +140,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   SegTot t{0u, 0u, 0ull, 0ull};
-  for (uint64_t wb = w0; wb < w1; wb += 32) {
-    const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
-    unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
-    while (nz) {  // 4 non-zero words at a time: their col[] loads are in flight together
-      ull c0[4], c1[4];
+  for (uint64_t w = w0 + lane; w < w1; w += 32) {
+    uint32_t x = __ldg(bm + w);
+    while (x) {  // 4 set bits at a time: their col[] loads are in flight together
+      ull dd[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int jw = nz ? __ffs(nz) - 1 : -1;
-        nz &= nz ? nz - 1 : 0u;
-        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
-        const bool bit = jw >= 0 && ((xw >> lane) & 1u);
-        const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
-        c0[b] = bit ? __ldg(col + u) : 0ull;
-        c1[b] = bit ? __ldg(col + u + 1) : 0ull;
+      for (int q = 0; q < 4; ++q) {
+        const int b = x ? __ffs(x) - 1 : -1;
+        x &= x ? x - 1 : 0u;
+        const uint64_t u = w * 32 + (b < 0 ? 0 : b);
+        dd[q] = b < 0 ? 0ull : __ldg(col + u + 1) - __ldg(col + u);
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const ull d = c1[b] - c0[b];
+      for (int q = 0; q < 4; ++q) {
+        const ull d = dd[q];
         if (d >= half) {
           t.na += (unsigned)((d + tm) >> tile_shift);
           t.ls += d;
@@ -188,7 +186,7 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   info->newv = 0;
   // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
   // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-  // the scan (P2) is used when that is <= p2_factor (default 4); otherwise (small frontiers,
+  // the scan (P2) is used when that is <= p2_factor (default 32); otherwise (small frontiers,
   // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).  P2 also when
   // few rows remain to be discovered (the scans are then few, whatever their length):
   // remaining = rows with entries - rows discovered so far (an estimate on this rank).
@@ -207,6 +205,9 @@ size_t seg_scan_tmp_bytes(uint64_t nseg) {
   return bytes;
 }
 
+// Emit pass: same word ownership; per chunk of 32 words each lane totals its word, one warp
+// exclusive scan per chunk gives every lane its list / edge / long-tile positions, then the
+// lane writes its columns in ascending order.
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                              uint64_t nseg, const ull* __restrict__ col,
                                                              const SegTot* seg_off, uint32_t* flist, ull* rowoff,
@@ -222,43 +223,50 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   ull e = o.ss;       // next short edge position
   uint64_t a = o.na;  // next long-tile position
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
-  const unsigned lt = lanemask_lt();
   unsigned nlongcols = 0;
-  for (uint64_t wb = w0; wb < w1; wb += 32) {
-    const uint32_t x = (wb + lane < w1) ? __ldg(bm + wb + lane) : 0u;
-    unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
-    while (nz) {  // 4 non-zero words at a time: their col[] loads are in flight together
-      int jwb[4];
-      ull c0b[4], c1b[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int jw = nz ? __ffs(nz) - 1 : -1;
-        nz &= nz ? nz - 1 : 0u;
-        jwb[b] = jw;
-        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
-        const bool bit = jw >= 0 && ((xw >> lane) & 1u);
-        const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
-        c0b[b] = bit ? __ldg(col + u) : 0ull;
-        c1b[b] = bit ? __ldg(col + u + 1) : 0ull;
+  const unsigned lt = lanemask_lt();
+  auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt) {
+    if (nt <= 8) {
+      for (unsigned q = 0; q < nt; ++q) {
+        const ull pos = c0 + ((ull)q << tile_shift);
+        const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+        tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
       }
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (jwb[b] < 0) break;  // warp-uniform
-        const uint64_t u = (wb + jwb[b]) * 32 + lane;
-        const ull c0 = c0b[b], d = c1b[b] - c0b[b];
+    } else {  // hub column: its tiles are written by k_tile_fill
+      const ull slot = atomicAdd(&info->nlong, 1ull);
+      longlist[2 * slot] = make_uint4((uint32_t)pa, nt, (uint32_t)u, (uint32_t)(pa >> 32));
+      longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
+    }
+  };
+  for (uint64_t wb = w0; wb < w1; wb += 32) {
+    const uint64_t w = wb + lane;
+    const uint32_t x = (w < w1) ? __ldg(bm + w) : 0u;
+    const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
+    if (nbits >= 96) {
+      // dense chunk: word by word, lane b handles bit b (coalesced col reads and list writes)
+      unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
+      while (nz) {
+        const int jw = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
+        const uint64_t u = (wb + jw) * 32 + lane;
+        ull c0 = 0, d = 0;
+        if ((xw >> lane) & 1u) {
+          c0 = __ldg(col + u);
+          d = __ldg(col + u + 1) - c0;
+        }
         const bool isl = d >= half;
-        const ull ds = isl ? 0ull : d;
+        const unsigned ds = isl ? 0u : (unsigned)d;  // short degree < TILE/2
         const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
         const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
-        ull inc = ds;     // inclusive warp scan of short degrees
-        unsigned ia = na; // inclusive warp scan of long-tile counts
+        unsigned inc = ds, ia = na;  // inclusive warp scans
 #pragma unroll
         for (int s2 = 1; s2 < 32; s2 <<= 1) {
-          const ull y = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
-          const unsigned ya = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
+          const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
+          const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
           if (lane >= s2) {
-            inc += y;
-            ia += ya;
+            inc += y1;
+            ia += y2;
           }
         }
         if (ds) {
@@ -267,29 +275,93 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
           flist[pos] = (uint32_t)u;
           rowoff[pos] = c0;
           cumul[pos] = eb;
-          // a short column spans at most two tiles
           for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
         }
         if (isl) {
-          const uint64_t pa = a + ia - na;
-          if (na <= 8) {
-            for (unsigned q = 0; q < na; ++q) {
-              const ull pos = c0 + ((ull)q << tile_shift);
-              const ull len = min(d - ((ull)q << tile_shift), tm + 1);
-              tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
-            }
-          } else {  // hub column: its tiles are written by k_tile_fill
-            const ull slot = atomicAdd(&info->nlong, 1ull);
-            longlist[2 * slot] = make_uint4((uint32_t)pa, na, (uint32_t)u, (uint32_t)(pa >> 32));
-            longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
-          }
+          emit_long(u, c0, d, a + ia - na, na);
           ++nlongcols;
         }
         k += __popc(smask);
         e += __shfl_sync(0xFFFFFFFFu, inc, 31);
         a += __shfl_sync(0xFFFFFFFFu, ia, 31);
       }
+      continue;
     }
+    // lane totals of its word
+    unsigned cs = 0, na = 0;
+    ull ss = 0;
+    for (uint32_t y = x; y;) {  // 4 set bits at a time
+      ull dd[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int b = y ? __ffs(y) - 1 : -1;
+        y &= y ? y - 1 : 0u;
+        const uint64_t u = w * 32 + (b < 0 ? 0 : b);
+        dd[q] = b < 0 ? 0ull : __ldg(col + u + 1) - __ldg(col + u);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const ull d = dd[q];
+        if (d >= half) na += (unsigned)((d + tm) >> tile_shift);
+        else if (d) {
+          cs += 1u;
+          ss += d;
+        }
+      }
+    }
+    // warp exclusive scans of the lane totals
+    unsigned ics = cs, ina = na;
+    ull iss = ss;
+#pragma unroll
+    for (int s2 = 1; s2 < 32; s2 <<= 1) {
+      const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, ics, s2);
+      const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ina, s2);
+      const ull y3 = __shfl_up_sync(0xFFFFFFFFu, iss, s2);
+      if (lane >= s2) {
+        ics += y1;
+        ina += y2;
+        iss += y3;
+      }
+    }
+    uint64_t kk = k + ics - cs;
+    ull ee = e + iss - ss;
+    uint64_t aa = a + ina - na;
+    for (uint32_t y = x; y;) {
+      int bq[4];
+      ull cq[4], dq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // 4 set bits at a time: loads in flight together
+        const int b = y ? __ffs(y) - 1 : -1;
+        y &= y ? y - 1 : 0u;
+        bq[q] = b;
+        const uint64_t u = w * 32 + (b < 0 ? 0 : b);
+        cq[q] = b < 0 ? 0ull : __ldg(col + u);
+        dq[q] = b < 0 ? 0ull : __ldg(col + u + 1) - cq[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+      if (bq[q] < 0) break;
+      const uint64_t u = w * 32 + bq[q];
+      const ull c0 = cq[q], d = dq[q];
+      if (d >= half) {
+        const unsigned nt = (unsigned)((d + tm) >> tile_shift);
+        emit_long(u, c0, d, aa, nt);
+        aa += nt;
+        ++nlongcols;
+      } else if (d) {
+        flist[kk] = (uint32_t)u;
+        rowoff[kk] = c0;
+        cumul[kk] = ee;
+        // a short column spans at most two tiles
+        for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) tile_k[t] = (uint32_t)kk;
+        ++kk;
+        ee += d;
+      }
+      }
+    }
+    k += __shfl_sync(0xFFFFFFFFu, ics, 31);
+    e += __shfl_sync(0xFFFFFFFFu, iss, 31);
+    a += __shfl_sync(0xFFFFFFFFu, ina, 31);
   }
 #pragma unroll
   for (int s2 = 16; s2; s2 >>= 1) nlongcols += __shfl_xor_sync(0xFFFFFFFFu, nlongcols, s2);
@@ -325,9 +397,9 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0ull, 0ull},
                                  (uint64_t)nseg + 1, s);
   static ull p2_factor = 0;
-  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 4)
+  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 32)
     const char* env = getenv("BFS200_P2_FACTOR");
-    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 4ull;
+    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 32ull;
   }
   k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
