@@ -188,7 +188,7 @@ def run_ours(args, rank, world, local_rank):
     k1 = M * (rank + 1) // world
     ds, dd = inputs.generate_device(scale, k0=k0, count=k1 - k0, device=dev)
     stream = torch.cuda.current_stream(dev)
-    opts = bfs.make_opts(edges_per_thread=args.E, phase_timing=True, stream=stream.cuda_stream)
+    opts = bfs.make_opts(edges_per_thread=args.E, phase_timing=not args.no_phase_timing, stream=stream.cuda_stream)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -227,6 +227,7 @@ def run_ours(args, rank, world, local_rank):
 
     times, mcomps, launches = [], [], 0
     exp_bytes, exp_ms, lvl_tot = 0.0, 0.0, 0
+    tail = {"finalize": 0.0, "resolve": 0.0}
     phase = {"expand_comm": 0.0, "scan": 0.0, "expand": 0.0, "parent": 0.0, "fold_comm": 0.0, "update": 0.0,
              "allreduce": 0.0}
     with ClockSampler(local_rank) as clk:
@@ -243,7 +244,9 @@ def run_ours(args, rank, world, local_rank):
             t_ms = max_over_ranks(ev0.elapsed_time(ev1))
             times.append(t_ms)
             launches += st.kernel_launches
-            recs = g.level_times()
+            tail["finalize"] += st.finalize_ms
+            tail["resolve"] += st.resolve_ms
+            recs = g.level_times() if not args.no_phase_timing else []
             lvl_tot += len(recs)
             for rec in recs:
                 for key in phase:
@@ -301,7 +304,8 @@ def run_ours(args, rank, world, local_rank):
                      "alg_bytes_per_step": exp_bytes / max(1, args.steps),
                      "kernel_ms_per_step": per_rank_exp_ms / max(1, args.steps),
                      "kernel_share_of_step": (per_rank_exp_ms / max(1, args.steps)) / step_ms},
-        "phase_ms_per_step": {k: v / max(1, args.steps) for k, v in phase.items()},
+        "phase_ms_per_step": {**{k: v / max(1, args.steps) for k, v in phase.items()},
+                              **{k: v / max(1, args.steps) for k, v in tail.items()}},
         "levels_per_step": lvl_tot / max(1, args.steps),
         "clocks": clocks,
         "graph": {"nverts": n, "tuples": M, "nnz_rank0": int(info.nnz_local), "build_s": t_build,
@@ -323,6 +327,7 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--E", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-phase-timing", action="store_true", help="(diagnostic) no per-phase events")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

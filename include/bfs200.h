@@ -93,6 +93,8 @@ typedef struct {
   uint64_t reached;          /* owned vertices reached (level >= 0)                        */
   uint64_t bytes_exchanged;  /* bytes sent by this process's ranks over the transport      */
   uint64_t kernel_launches;  /* libbfs200 kernels launched by the call (CUB/NCCL excluded)  */
+  double finalize_ms;        /* output write (phase_timing only, else 0)                   */
+  double resolve_ms;         /* end-of-search parent exchange, C > 1 (phase_timing only)   */
 } bfs_stats;
 
 /* Per-level phase times (milliseconds, CUDA events) of the last run with phase_timing. */

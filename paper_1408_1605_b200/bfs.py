@@ -45,7 +45,8 @@ class Info(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int), ("edges_scanned", ctypes.c_uint64),
                 ("frontier_columns", ctypes.c_uint64), ("reached", ctypes.c_uint64),
-                ("bytes_exchanged", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64)]
+                ("bytes_exchanged", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("finalize_ms", ctypes.c_double), ("resolve_ms", ctypes.c_double)]
 
 
 class LevelRecord(ctypes.Structure):

@@ -124,6 +124,7 @@ struct Graph {
   bool has_run = false;
   // phase-timing events: [level][phase boundary]
   std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> tail_ev;  // finalize / parent-resolution events (phase_timing)
   int ev_levels = 0;
   std::vector<uint64_t> lvl_frontier, lvl_edges;
 };

@@ -227,6 +227,8 @@ static void release_graph(Graph* G) {
   G->allocs.clear();
   for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
   G->ev.clear();
+  for (cudaEvent_t e : G->tail_ev) cudaEventDestroy(e);
+  G->tail_ev.clear();
   if (G->h_infos) cudaFreeHost(G->h_infos);
   if (G->h_scratch) cudaFreeHost(G->h_scratch);
   if (G->rowc) ncclCommDestroy(G->rowc);
@@ -466,14 +468,24 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   const size_t nl = G.ranks.size();
   const bool par_is_dev = is_device_ptr(parent), lev_is_dev = is_device_ptr(level);
   std::vector<int64_t*> par_dev(nl, nullptr);
+  if (G.opts.phase_timing) {
+    for (int q = (int)G.tail_ev.size(); q < 3; ++q) {
+      cudaEvent_t ev;
+      CKR(cudaEventCreate(&ev));
+      G.tail_ev.push_back(ev);
+    }
+    CKR(cudaEventRecord(G.tail_ev[0], s));
+  }
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : rk.parent_tmp;
     CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr, s));
   }
+  if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
   if (g.C > 1 && parent) {
     if ((rc = resolve_parents(G, par_dev.data()))) return rc;
   }
+  if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[2], s));
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     if (parent && !par_is_dev)
@@ -491,6 +503,13 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       stats->frontier_columns += G.lvl_frontier[l];
     }
     stats->bytes_exchanged = bytes;
+    if (G.opts.phase_timing) {  // the stream is synchronised: reading the events costs nothing
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, G.tail_ev[0], G.tail_ev[1]);
+      cudaEventElapsedTime(&b, G.tail_ev[1], G.tail_ev[2]);
+      stats->finalize_ms = a;
+      stats->resolve_ms = b;
+    }
     stats->reached = 0;
     // own kernels: seed (owner only) + per level and local rank scan(4) + expand + parent +
     // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals,
