@@ -15,6 +15,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -290,7 +291,13 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   G.g.R = R;
   G.g.C = C;
   G.g.block = G.g.npad / P;
-  G.hot_h = G.g.block < (1ull << 23) ? G.g.block : (1ull << 23);  // degree-ordered prefix
+  {  // degree-ordered prefix per vertex block; BFS200_HOT_PREFIX overrides (experiments)
+    const char* env = getenv("BFS200_HOT_PREFIX");
+    const uint64_t want = (env && atoll(env) > 0) ? (uint64_t)atoll(env) : (1ull << 22);
+    G.hot_h = G.g.block < want ? G.g.block : want;
+    G.hot_h &= ~31ull;
+    if (!G.hot_h) G.hot_h = G.g.block;
+  }
   G.ntuples = nedges;
   CKR(cudaMallocHost(&G.h_scratch, 16 * sizeof(ull)));
   {
@@ -466,7 +473,10 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   G.last_levels = nlev;
   // outputs
   const size_t nl = G.ranks.size();
-  const bool par_is_dev = is_device_ptr(parent), lev_is_dev = is_device_ptr(level);
+  // the finalize kernel writes 16-byte vectors: unaligned device outputs go through the staging
+  // buffers like host outputs (then one copy)
+  const bool par_is_dev = is_device_ptr(parent) && (((uintptr_t)parent & 15) == 0);
+  const bool lev_is_dev = is_device_ptr(level) && (((uintptr_t)level & 15) == 0);
   std::vector<int64_t*> par_dev(nl, nullptr);
   if (G.opts.phase_timing) {
     for (int q = (int)G.tail_ev.size(); q < 3; ++q) {
@@ -489,9 +499,9 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     if (parent && !par_is_dev)
-      CKR(cudaMemcpyAsync(parent + k * g.block, rk.parent_tmp, g.block * 8, cudaMemcpyDeviceToHost, s));
+      CKR(cudaMemcpyAsync(parent + k * g.block, rk.parent_tmp, g.block * 8, cudaMemcpyDefault, s));
     if (level && !lev_is_dev)
-      CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDeviceToHost, s));
+      CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDefault, s));
   }
   CKR(cudaStreamSynchronize(s));
   G.has_run = true;

@@ -1030,27 +1030,37 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
 // For owned t: unreached (visited bit clear) -> level -1, parent -1; reached with the winner
 // column == own column (always when C == 1) -> parent = pred of the own row segment; other
 // reached vertices are filled by the resolution exchange (k_resp_scatter).
-// p indexes the relabeled owned offsets (state, read coalesced); t = inv_own[p] the ORIGINAL one
-// (outputs; identity outside the relabeled prefix, so most writes are coalesced too).
+// t indexes the ORIGINAL owned offsets (outputs, written coalesced); p = fwd_own[t] the relabeled
+// one (state; identity outside the relabeled prefix and the slots it displaced).  Four outputs
+// per thread with 16-byte loads and stores (block is a multiple of 32).
 __global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const uint32_t* pred_own,
-                           const uint8_t* winner, const uint32_t* inv_own, int j, uint64_t block, int64_t* parent_out,
+                           const uint8_t* winner, const uint32_t* fwd_own, int j, uint64_t block, int64_t* parent_out,
                            int32_t* level_out) {
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= block) return;
-  const uint32_t t = inv_own[p];
-  const bool reached = (vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
-  if (parent_out) {
-    int64_t q = -1;
-    if (reached && (!winner || winner[p] == (uint8_t)j)) q = (int64_t)pred_own[p];
-    parent_out[t] = q;
+  const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (t0 >= block) return;
+  const uint4 p4 = *reinterpret_cast<const uint4*>(fwd_own + t0);
+  const uint32_t pp[4] = {p4.x, p4.y, p4.z, p4.w};
+  int64_t q[4];
+  int32_t l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t p = pp[k];
+    const bool reached = (vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
+    q[k] = (reached && (!winner || winner[p] == (uint8_t)j)) ? (int64_t)pred_own[p] : -1;
+    l[k] = reached ? level[p] : -1;
   }
-  if (level_out) level_out[t] = reached ? level[p] : -1;
+  if (parent_out) {
+    longlong2* po = reinterpret_cast<longlong2*>(parent_out + t0);
+    po[0] = make_longlong2(q[0], q[1]);
+    po[1] = make_longlong2(q[2], q[3]);
+  }
+  if (level_out) *reinterpret_cast<int4*>(level_out + t0) = make_int4(l[0], l[1], l[2], l[3]);
 }
 
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
-  const unsigned grid = (unsigned)((g.block + 255) / 256);
+  const unsigned grid = (unsigned)((g.block / 4 + 255) / 256);
   k_finalize<<<grid, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.level,
-                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.inv_own, rk.j,
+                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.fwd_own, rk.j,
                                   g.block, parent_out, level_out);
   return cudaGetLastError();
 }

@@ -233,3 +233,19 @@ def test_s26_bench_config_graph500_valid(bfs):
         mask = oracle.validate(n, hs, hd, r, lv[:n], pa[:n])
         assert mask == 0, oracle.failed_names(mask)
         assert g.mcomp() == int(np.count_nonzero(lv[hs] >= 0))
+
+
+def test_unaligned_device_outputs(bfs):
+    """Device output buffers that are not 16-byte aligned take the staging path."""
+    scale = 12
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    og = oracle.Graph(n, s, d)
+    g = make_graph(bfs, s, d, n)
+    r = inputs.sample_roots(n, 1, inputs.nonisolated_mask(n, s, d))[0]
+    ol, op = og.bfs(r)
+    pbuf = torch.empty(g.info.nout + 1, dtype=torch.int64, device="cuda")
+    lbuf = torch.empty(g.info.nout + 1, dtype=torch.int32, device="cuda")
+    pd, ld = pbuf[1:], lbuf[1:]  # 8- and 4-byte offsets
+    g.run(r, pd, ld)
+    assert np.array_equal(ld.cpu().numpy()[:n], ol) and np.array_equal(pd.cpu().numpy()[:n], op)

@@ -35,7 +35,8 @@ level = torch.empty(g.info.nout, dtype=torch.int32, device="cuda")
 for r in roots:
     st = g.run(r, parent, level)
     recs = g.level_times()
-    print(f"root {r}: levels {st.nlevels} edges {st.edges_scanned} mcomp {g.mcomp()}")
+    print(f"root {r}: levels {st.nlevels} edges {st.edges_scanned} mcomp {g.mcomp()} "
+          f"finalize {st.finalize_ms:.3f} ms resolve {st.resolve_ms:.3f} ms")
     for i, x in enumerate(recs):
         print(f"  L{i}: frontier {x.frontier:>10} edges {x.edges:>12} scan {x.scan:7.3f} expand {x.expand:7.3f} "
               f"parent {x.parent:6.3f} update {x.update:6.3f} ms  -> "
