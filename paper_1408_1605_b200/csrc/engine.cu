@@ -354,7 +354,7 @@ static inline int ev_rec(Graph& G, int level, int p) {
 }
 
 // ------------------------------------------------------------------ parent resolution (C > 1)
-static int resolve_parents(Graph& G, int64_t* const* par_dev) {
+static int resolve_parents(Graph& G) {
   const Geom& g = G.g;
   const uint64_t W = g.words_block();
   const int C = g.C;
@@ -416,8 +416,7 @@ static int resolve_parents(Graph& G, int64_t* const* par_dev) {
     }
     NKR(ncclGroupEnd());
   }
-  for (size_t k = 0; k < nl; ++k) CKR(launch_resp_scatter(g, G.ranks[k], par_dev[k], s));
-  return BFS_OK;
+  return BFS_OK;  // k_finalize reads the answers (no separate scatter)
 }
 
 // ------------------------------------------------------------------ one BFS
@@ -486,14 +485,14 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
     CKR(cudaEventRecord(G.tail_ev[0], s));
   }
+  if (g.C > 1 && parent) {
+    if ((rc = resolve_parents(G))) return rc;
+  }
+  if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : rk.parent_tmp;
     CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr, s));
-  }
-  if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
-  if (g.C > 1 && parent) {
-    if ((rc = resolve_parents(G, par_dev.data()))) return rc;
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[2], s));
   for (size_t k = 0; k < nl; ++k) {
@@ -517,15 +516,15 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, G.tail_ev[0], G.tail_ev[1]);
       cudaEventElapsedTime(&b, G.tail_ev[1], G.tail_ev[2]);
-      stats->finalize_ms = a;
-      stats->resolve_ms = b;
+      stats->resolve_ms = a;
+      stats->finalize_ms = b;
     }
     stats->reached = 0;
     // own kernels: seed (owner only) + per level and local rank scan(4) + expand + parent +
-    // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals,
-    // resp_pack, resp_scatter.
+    // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals and
+    // resp_pack.
     const uint64_t nl = G.ranks.size();
-    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 5 : 0);
+    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0);
   }
   return BFS_OK;
 }

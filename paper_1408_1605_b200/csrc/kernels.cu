@@ -1029,25 +1029,50 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
 // ------------------------------------------------------------------ outputs
 // For owned t: unreached (visited bit clear) -> level -1, parent -1; reached with the winner
 // column == own column (always when C == 1) -> parent = pred of the own row segment; other
-// reached vertices are filled by the resolution exchange (k_resp_scatter).
+// reached vertices take the answers of the resolution exchange (see k_finalize).
 // t indexes the ORIGINAL owned offsets (outputs, written coalesced); p = fwd_own[t] the relabeled
 // one (state; identity outside the relabeled prefix and the slots it displaced).  Four outputs
-// per thread with 16-byte loads and stores (block is a multiple of 32).
-__global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const uint32_t* pred_own,
-                           const uint8_t* winner, const uint32_t* fwd_own, int j, uint64_t block, int64_t* parent_out,
-                           int32_t* level_out) {
+// per thread with 16-byte loads and stores (block is a multiple of 32).  With C > 1 a vertex
+// whose winner column c differs from j takes its parent from the answers of P_ic: position =
+// rank of its bit among the requests sent to c (exclusive popcount scan off_req + in-word popc).
+struct FinalizeArgs {
+  const uint32_t* vd_own;
+  const int32_t* level;
+  const uint32_t* pred_own;
+  const uint8_t* winner;  // null when C == 1
+  const uint32_t* fwd_own;
+  const uint32_t* req;      // [C*W] request bitmaps
+  const uint32_t* off_req;  // exclusive popcount scan of req
+  const uint32_t* respin;   // answers, segment c at c*block
+  int j;
+  uint64_t block, W;
+};
+
+__global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_out) {
   const uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (t0 >= block) return;
-  const uint4 p4 = *reinterpret_cast<const uint4*>(fwd_own + t0);
+  if (t0 >= a.block) return;
+  const uint4 p4 = *reinterpret_cast<const uint4*>(a.fwd_own + t0);
   const uint32_t pp[4] = {p4.x, p4.y, p4.z, p4.w};
   int64_t q[4];
   int32_t l[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t p = pp[k];
-    const bool reached = (vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
-    q[k] = (reached && (!winner || winner[p] == (uint8_t)j)) ? (int64_t)pred_own[p] : -1;
-    l[k] = reached ? level[p] : -1;
+    const bool reached = (a.vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
+    int64_t v = -1;
+    if (reached) {
+      const int c = a.winner ? (int)a.winner[p] : a.j;
+      if (c == a.j) {
+        v = (int64_t)a.pred_own[p];
+      } else {
+        const uint64_t wi = (uint64_t)c * a.W + (p >> 5);
+        const uint32_t below = a.req[wi] & ((1u << (p & 31)) - 1u);
+        const uint64_t pos = a.off_req[wi] - a.off_req[(uint64_t)c * a.W] + __popc(below);
+        v = (int64_t)a.respin[(uint64_t)c * a.block + pos];
+      }
+    }
+    q[k] = v;
+    l[k] = reached ? a.level[p] : -1;
   }
   if (parent_out) {
     longlong2* po = reinterpret_cast<longlong2*>(parent_out + t0);
@@ -1058,10 +1083,20 @@ __global__ void k_finalize(const uint32_t* vd_own, const int32_t* level, const u
 }
 
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
+  FinalizeArgs a;
+  a.vd_own = rk.vd + 2 * (uint64_t)rk.j * g.words_block();
+  a.level = rk.level;
+  a.pred_own = rk.pred + (uint64_t)rk.j * g.block;
+  a.winner = (g.C > 1 && parent_out) ? rk.winner : nullptr;  // parents of other columns need resolution
+  a.fwd_own = rk.fwd_own;
+  a.req = rk.req;
+  a.off_req = rk.off_req;
+  a.respin = rk.respin;
+  a.j = rk.j;
+  a.block = g.block;
+  a.W = g.words_block();
   const unsigned grid = (unsigned)((g.block / 4 + 255) / 256);
-  k_finalize<<<grid, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.level,
-                                  rk.pred + (uint64_t)rk.j * g.block, g.C > 1 ? rk.winner : nullptr, rk.fwd_own, rk.j,
-                                  g.block, parent_out, level_out);
+  k_finalize<<<grid, 256, 0, s>>>(a, parent_out, level_out);
   return cudaGetLastError();
 }
 
@@ -1129,31 +1164,6 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t n = W * g.C;
   k_resp_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.reqin, rk.off_in, rk.pred, rk.resp, W, g.block, g.C,
                                                           rk.j);
-  return cudaGetLastError();
-}
-
-// owner: scatter the answers for its requests (req_off holds the popc scan of req here)
-__global__ void k_resp_scatter(const uint32_t* req, const uint32_t* off, const uint32_t* respin, int64_t* parent,
-                               const uint32_t* inv_own, uint64_t W, uint64_t block, int C, int j) {
-  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= W * (uint64_t)C) return;
-  const int c = (int)(gid / W);
-  if (c == j) return;
-  const uint64_t w = gid - (uint64_t)c * W;
-  uint32_t b = req[gid];
-  uint64_t pos = off[gid] - off[(uint64_t)c * W];
-  while (b) {
-    const int bit = __ffs(b) - 1;
-    b &= b - 1;
-    parent[inv_own[w * 32 + bit]] = (int64_t)respin[(uint64_t)c * block + pos++];
-  }
-}
-
-cudaError_t launch_resp_scatter(const Geom& g, Rank& rk, int64_t* parent_out, cudaStream_t s) {
-  const uint64_t W = g.words_block();
-  const uint64_t n = W * g.C;
-  k_resp_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.req, rk.off_req, rk.respin, parent_out, rk.inv_own,
-                                                             W, g.block, g.C, rk.j);
   return cudaGetLastError();
 }
 

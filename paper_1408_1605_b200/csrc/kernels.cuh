@@ -25,13 +25,12 @@ cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s);
 // Finalize: parent/level outputs for owned vertices whose parent is local.
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s);
 
-// Parent resolution (C > 1): build request bitmaps, answer requests, scatter answers.
+// Parent resolution (C > 1): build request bitmaps and answer requests (k_finalize reads them).
 cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s);
 cudaError_t launch_popc_scan(const uint32_t* bits, uint32_t* off, uint64_t nwords, void* tmp, size_t tmp_bytes,
                              cudaStream_t s);
 size_t popc_scan_tmp_bytes(uint64_t nwords);
 cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s);
-cudaError_t launch_resp_scatter(const Geom& g, Rank& rk, int64_t* parent_out, cudaStream_t s);
 
 cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s);
 
