@@ -36,6 +36,17 @@ struct LevelInfo {
   unsigned long long pad[6];
 };
 
+// Device-side level loop state (the loop may run as a CUDA-graph WHILE node).
+struct LevelCtrl {
+  uint32_t lvl;   // level being assigned (1 for the root's neighbours)
+  uint32_t nlev;  // levels executed
+  uint32_t done;
+  uint32_t pad;
+  unsigned long long total_new;  // vertices discovered by the last level (all ranks)
+  unsigned long long lvl_frontier[kMaxLevels];
+  unsigned long long lvl_edges[kMaxLevels];
+};
+
 // Geometry of the 2D partition (index maps SPEC.md S:109-148).
 struct Geom {
   uint64_t nverts, npad, block;
@@ -125,6 +136,16 @@ struct Graph {
   // phase-timing events: [level][phase boundary]
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> tail_ev;  // finalize / parent-resolution events (phase_timing)
+  // level loop as a CUDA graph (one WHILE node whose body is one level), built on first use
+  LevelCtrl* d_ctrl = nullptr;
+  LevelCtrl* h_ctrl = nullptr;  // pinned mirror
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  cudaStream_t graph_stream = nullptr;
+  int graph_E = 0;
+  bool graph_failed = false;
+  int runs = 0;
   int ev_levels = 0;
   std::vector<uint64_t> lvl_frontier, lvl_edges;
 };

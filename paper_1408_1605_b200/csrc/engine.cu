@@ -219,6 +219,8 @@ static int alloc_state(Graph& G, Rank& rk) {
   return BFS_OK;
 }
 
+static void drop_graph(Graph& G);
+
 // release every resource held by *G (the Graph object itself is owned by bfs_graph)
 static void release_graph(Graph* G) {
   if (!G) return;
@@ -230,7 +232,10 @@ static void release_graph(Graph* G) {
   G->ev.clear();
   for (cudaEvent_t e : G->tail_ev) cudaEventDestroy(e);
   G->tail_ev.clear();
+  drop_graph(*G);
   if (G->h_infos) cudaFreeHost(G->h_infos);
+  if (G->h_ctrl) cudaFreeHost(G->h_ctrl);
+  G->h_ctrl = nullptr;
   if (G->h_scratch) cudaFreeHost(G->h_scratch);
   if (G->rowc) ncclCommDestroy(G->rowc);
   if (G->colc) ncclCommDestroy(G->colc);
@@ -324,6 +329,9 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   if (rc) return rc;
   rc = G_alloc(G, (void**)&G.infos, nlocal * sizeof(LevelInfo));
   if (rc) return rc;
+  rc = G_alloc(G, (void**)&G.d_ctrl, sizeof(LevelCtrl));
+  if (rc) return rc;
+  CKR(cudaMallocHost(&G.h_ctrl, sizeof(LevelCtrl)));
   CKR(cudaMallocHost(&G.h_infos, nlocal * sizeof(LevelInfo)));
   for (int k = 0; k < nlocal; ++k) {
     G.ranks[k].info = G.infos + k;
@@ -420,11 +428,72 @@ static int resolve_parents(Graph& G) {
 }
 
 // ------------------------------------------------------------------ one BFS
-static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
+// One level of Alg.2, enqueued on the graph's stream without host synchronisation:
+// expand exchange, K3 scan, K1 expansion, K4 parent claim, fold exchange, K2 update,
+// termination all-reduce and the device-side level bookkeeping.  use_cond: the call is being
+// captured into the body of the CUDA-graph WHILE node (no phase events then).
+static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const Geom& g = G.g;
   cudaStream_t s = G.stream;
   const int E = G.opts.edges_per_thread;
   const uint32_t tile_edges = expand_tile_edges(E);
+  const bool ev = !use_cond;
+  int rc;
+  if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
+  if ((rc = expand_exchange(G))) return rc;
+  if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
+  for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
+  if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
+  for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, s));
+  if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
+  for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
+  if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
+  if ((rc = fold_exchange(G))) return rc;
+  if (ev && (rc = ev_rec(G, nlev, 5))) return rc;
+  for (Rank& rk : G.ranks) CKR(launch_update(g, rk, G.d_ctrl, s));
+  if (ev && (rc = ev_rec(G, nlev, 6))) return rc;
+  if (G.world_size > 1) NKR(ncclAllReduce(&G.infos[0].newv, &G.infos[0].newv, 1, ncclUint64, ncclSum, G.world, s));
+  CKR(launch_level_end(G.d_ctrl, G.infos, (int)G.ranks.size(), G.world_size > 1, G.cond, use_cond, s));
+  if (ev && (rc = ev_rec(G, nlev, 7))) return rc;
+  return BFS_OK;
+}
+
+static void drop_graph(Graph& G) {
+  if (G.gexec) cudaGraphExecDestroy(G.gexec);
+  if (G.graph) cudaGraphDestroy(G.graph);
+  G.gexec = nullptr;
+  G.graph = nullptr;
+}
+
+// The level loop as one CUDA graph: a WHILE conditional node whose body is one captured level;
+// k_level_end sets the condition (no host round trip per level).
+static int build_level_graph(Graph& G) {
+  drop_graph(G);
+  CKR(cudaGraphCreate(&G.graph, 0));
+  CKR(cudaGraphConditionalHandleCreate(&G.cond, G.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = G.cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CKR(cudaGraphAddNode(&node, G.graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CKR(cudaStreamBeginCaptureToGraph(G.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  int rc = enqueue_level(G, true, 0);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(G.stream, &captured);
+  if (rc) return rc;
+  CKR(e);
+  CKR(cudaGraphInstantiate(&G.gexec, G.graph, 0));
+  G.graph_stream = G.stream;
+  G.graph_E = G.opts.edges_per_thread;
+  return BFS_OK;
+}
+
+static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
+  const Geom& g = G.g;
+  cudaStream_t s = G.stream;
   const uint64_t W = g.words_block();
   const uint64_t owner = root / g.block;
   bool owner_local = false;
@@ -432,44 +501,33 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     owner_local |= (uint64_t)rk.r == owner;
     CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, s));
   }
-  G.lvl_frontier.clear();
-  G.lvl_edges.clear();
-  ull bytes = 0;
-  int lvl = 1, nlev = 0;
+  CKR(launch_level_begin(G.d_ctrl, s));
   int rc;
-  for (;;) {
-    if (nlev >= kMaxLevels) return set_err(BFS_ESTATE, "level limit exceeded");
-    if ((rc = ev_rec(G, nlev, 0))) return rc;
-    if ((rc = expand_exchange(G))) return rc;
-    if ((rc = ev_rec(G, nlev, 1))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
-    if ((rc = ev_rec(G, nlev, 2))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, s));
-    if ((rc = ev_rec(G, nlev, 3))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
-    if ((rc = ev_rec(G, nlev, 4))) return rc;
-    if ((rc = fold_exchange(G))) return rc;
-    if ((rc = ev_rec(G, nlev, 5))) return rc;
-    for (Rank& rk : G.ranks) CKR(launch_update(g, rk, lvl, s));
-    if ((rc = ev_rec(G, nlev, 6))) return rc;
-    if (G.world_size > 1) NKR(ncclAllReduce(&G.infos[0].newv, &G.infos[0].newv, 1, ncclUint64, ncclSum, G.world, s));
-    CKR(cudaMemcpyAsync(G.h_infos, G.infos, G.ranks.size() * sizeof(LevelInfo), cudaMemcpyDeviceToHost, s));
-    if ((rc = ev_rec(G, nlev, 7))) return rc;
-    CKR(cudaStreamSynchronize(s));
-    ull total_new = 0, fr = 0, ed = 0;
-    for (size_t k = 0; k < G.ranks.size(); ++k) {
-      total_new += G.h_infos[k].newv;
-      fr += G.h_infos[k].n + G.h_infos[k].nlongcols;
-      ed += G.h_infos[k].edges;
+  // graph mode: no phase events, and not on the very first run (which initialises the kernels'
+  // launch attributes outside of any capture)
+  bool use_graph = !G.opts.phase_timing && !G.graph_failed && G.runs > 0;
+  if (use_graph && (!G.gexec || G.graph_stream != s || G.graph_E != G.opts.edges_per_thread)) {
+    if (build_level_graph(G) != BFS_OK) {
+      // orchestration fallback only (same kernels, host-driven loop); clear the sticky state
+      G.graph_failed = true;
+      G.broken = false;
+      cudaGetLastError();
+      drop_graph(G);
+      use_graph = false;
+      cudaStreamSynchronize(s);
     }
-    G.lvl_frontier.push_back(fr);
-    G.lvl_edges.push_back(ed);
-    bytes += (ull)G.ranks.size() * ((ull)(g.R - 1) + (ull)(g.C - 1)) * W * 4;
-    ++nlev;
-    if (total_new == 0) break;
-    ++lvl;
   }
-  G.last_levels = nlev;
+  if (use_graph) {
+    CKR(cudaGraphLaunch(G.gexec, s));
+  } else {
+    for (int nlev = 0;; ++nlev) {
+      if (nlev >= kMaxLevels) return set_err(BFS_ESTATE, "level limit exceeded");
+      if ((rc = enqueue_level(G, false, nlev))) return rc;
+      CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
+      CKR(cudaStreamSynchronize(s));
+      if (G.h_ctrl->done) break;
+    }
+  }
   // outputs
   const size_t nl = G.ranks.size();
   // the finalize kernel writes 16-byte vectors: unaligned device outputs go through the staging
@@ -503,7 +561,19 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDefault, s));
   }
   CKR(cudaStreamSynchronize(s));
+  // per-level statistics of the device-side loop
+  CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
+  CKR(cudaStreamSynchronize(s));
+  const int nlev = (int)G.h_ctrl->nlev;
+  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_frontier, G.d_ctrl->lvl_frontier, nlev * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_edges, G.d_ctrl->lvl_edges, nlev * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  CKR(cudaStreamSynchronize(s));
+  G.last_levels = nlev;
+  G.lvl_frontier.assign(G.h_ctrl->lvl_frontier, G.h_ctrl->lvl_frontier + nlev);
+  G.lvl_edges.assign(G.h_ctrl->lvl_edges, G.h_ctrl->lvl_edges + nlev);
+  const ull bytes = (ull)nlev * G.ranks.size() * ((ull)(g.R - 1) + (ull)(g.C - 1)) * W * 4;
   G.has_run = true;
+  ++G.runs;
   if (stats) {
     memset(stats, 0, sizeof *stats);
     stats->nlevels = nlev;
@@ -520,11 +590,12 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       stats->finalize_ms = b;
     }
     stats->reached = 0;
-    // own kernels: seed (owner only) + per level and local rank scan(4) + expand + parent +
-    // update, then finalize; with C > 1 the resolution adds req_build, 2 seg_totals and
-    // resp_pack.
+    // own kernels: seed (owner only), level_begin, per level level_end and per local rank
+    // scan(4) + expand + parent + update, then finalize; with C > 1 the resolution adds
+    // req_build, 2 seg_totals and resp_pack.
     const uint64_t nl = G.ranks.size();
-    stats->kernel_launches = (owner_local ? 1 : 0) + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0);
+    stats->kernel_launches =
+        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0);
   }
   return BFS_OK;
 }

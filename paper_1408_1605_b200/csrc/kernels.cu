@@ -976,8 +976,9 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
 // rows this rank discovered as visited so they are sent at most once.
 __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* recv, uint32_t* front_seg,
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
-                                                int j, int lvl) {
+                                                int j, const LevelCtrl* ctrl) {
   // grid: x over the words of one segment, y = segment m (no 64-bit division)
+  const int lvl = (int)ctrl->lvl;  // the level being assigned (device-side: the loop may be a graph)
   const int m = (int)blockIdx.y;
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t gid = (uint64_t)m * W + w;
@@ -1018,11 +1019,55 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&info->newv, (ull)cnt);
 }
 
-cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s) {
+cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s) {
   const uint64_t W = g.words_block();
   const dim3 grid((unsigned)((W + 255) / 256), (unsigned)g.C);
   k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
-                                g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, lvl);
+                                g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, ctrl);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ level control
+// End of a level: termination test on the total of new vertices (all local ranks; with NCCL the
+// update counter of rank 0's info has been all-reduced first), per-level statistics, lvl + 1,
+// and -- when the level loop is a CUDA-graph WHILE node -- the loop condition.
+__global__ void k_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal, int distributed,
+                            cudaGraphConditionalHandle cond, int use_cond) {
+  if (threadIdx.x != 0) return;
+  ull total = 0, fr = 0, ed = 0;
+  for (int k = 0; k < nlocal; ++k) {
+    total += distributed ? (k == 0 ? infos[0].newv : 0ull) : infos[k].newv;
+    fr += infos[k].n + infos[k].nlongcols;
+    ed += infos[k].edges;
+  }
+  const uint32_t l = ctrl->nlev;
+  if (l < kMaxLevels) {
+    ctrl->lvl_frontier[l] = fr;
+    ctrl->lvl_edges[l] = ed;
+  }
+  ctrl->nlev = l + 1;
+  ctrl->lvl += 1;
+  ctrl->total_new = total;
+  const bool done = total == 0 || l + 1 >= kMaxLevels;
+  ctrl->done = done ? 1u : 0u;
+  if (use_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
+}
+
+__global__ void k_level_begin(LevelCtrl* ctrl) {
+  ctrl->lvl = 1;
+  ctrl->nlev = 0;
+  ctrl->done = 0;
+  ctrl->total_new = 0;
+}
+
+cudaError_t launch_level_begin(LevelCtrl* ctrl, cudaStream_t s) {
+  k_level_begin<<<1, 1, 0, s>>>(ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal, bool distributed,
+                             cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s) {
+  k_level_end<<<1, 32, 0, s>>>(ctrl, infos, nlocal, distributed ? 1 : 0, cond, use_cond ? 1 : 0);
   return cudaGetLastError();
 }
 

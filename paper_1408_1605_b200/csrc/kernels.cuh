@@ -20,7 +20,12 @@ size_t seg_scan_tmp_bytes(uint64_t nseg);
 cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s);
 
 // K2: frontier update + pack; lvl is the level being assigned.
-cudaError_t launch_update(const Geom& g, Rank& rk, int lvl, cudaStream_t s);
+cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s);
+
+// Level control: reset (lvl = 1) and end-of-level bookkeeping / termination.
+cudaError_t launch_level_begin(LevelCtrl* ctrl, cudaStream_t s);
+cudaError_t launch_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal, bool distributed,
+                             cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s);
 
 // Finalize: parent/level outputs for owned vertices whose parent is local.
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s);
