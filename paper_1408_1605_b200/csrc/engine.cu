@@ -192,9 +192,9 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.tile_k, (rk.nnz / 32 + 2) * 4);          // short-edge tiles have >= 32 edges
   AL(rk.tileA, (3 * (rk.nnz / 32) + 64) * 16);    // long tiles: <= nnz/TILE + #long columns (d >= TILE/2)
   AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
-  AL(rk.seg_tot, (nseg + 1) * 24);
-  AL(rk.seg_off, (nseg + 1) * 24);
-  CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 24, G.stream));  // entry nseg stays zero
+  AL(rk.seg_tot, (nseg + 1) * 32);
+  AL(rk.seg_off, (nseg + 1) * 32);
+  CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
   rk.seg_tmp_bytes = seg_scan_tmp_bytes(nseg);
   AL(rk.seg_tmp, rk.seg_tmp_bytes);
   AL(rk.parent_tmp, g.block * 8);

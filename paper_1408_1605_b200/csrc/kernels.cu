@@ -118,13 +118,15 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
 struct SegTot {
   unsigned int cs;  // short columns
   unsigned int na;  // long-column tiles
+  unsigned int nh;  // hub columns (> 8 long tiles; their records are written by k_tile_fill)
+  unsigned int pad;
   ull ss;           // short edges
   ull ls;           // long edges
 };
-static_assert(sizeof(SegTot) == 24, "engine.cu allocates 24 B per segment");
+static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
 struct SegAdd {
   __device__ __forceinline__ SegTot operator()(const SegTot& a, const SegTot& b) const {
-    return SegTot{a.cs + b.cs, a.na + b.na, a.ss + b.ss, a.ls + b.ls};
+    return SegTot{a.cs + b.cs, a.na + b.na, a.nh + b.nh, 0u, a.ss + b.ss, a.ls + b.ls};
   }
 };
 
@@ -155,7 +157,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
       for (int q = 0; q < 4; ++q) {
         const ull d = dd[q];
         if (d >= half) {
-          t.na += (unsigned)((d + tm) >> tile_shift);
+          const unsigned nt = (unsigned)((d + tm) >> tile_shift);
+          t.na += nt;
+          t.nh += nt > 8 ? 1u : 0u;
           t.ls += d;
         } else if (d) {
           t.cs += 1u;
@@ -168,6 +172,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   for (int o = 16; o; o >>= 1) {
     t.cs += __shfl_xor_sync(0xFFFFFFFFu, t.cs, o);
     t.na += __shfl_xor_sync(0xFFFFFFFFu, t.na, o);
+    t.nh += __shfl_xor_sync(0xFFFFFFFFu, t.nh, o);
     t.ss += __shfl_xor_sync(0xFFFFFFFFu, t.ss, o);
     t.ls += __shfl_xor_sync(0xFFFFFFFFu, t.ls, o);
   }
@@ -193,7 +198,7 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   const ull edges = c.ss + c.ls, seen = info->disc_total;
   const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
   info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
-  info->nlong = 0;
+  info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
   info->nlongcols = 0;
   cumul[c.cs] = c.ss;
 }
@@ -201,13 +206,14 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
 size_t seg_scan_tmp_bytes(uint64_t nseg) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const SegTot*)nullptr, (SegTot*)nullptr, SegAdd(),
-                                 SegTot{0u, 0u, 0ull, 0ull}, (uint64_t)nseg + 1);
+                                 SegTot{0u, 0u, 0u, 0u, 0ull, 0ull}, (uint64_t)nseg + 1);
   return bytes;
 }
 
-// Emit pass: same word ownership; per chunk of 32 words each lane totals its word, one warp
-// exclusive scan per chunk gives every lane its list / edge / long-tile positions, then the
-// lane writes its columns in ascending order.
+// Emit pass: same word ownership.  Sparse chunks (< 96 set bits in 32 words): each lane totals
+// its word, one warp exclusive scan per chunk gives the lane its list / edge / long-tile / hub
+// positions, then the lane writes its columns in ascending order.  Dense chunks: word by word,
+// lane b handles bit b (coalesced col reads and list writes), col loads of 4 words in flight.
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                              uint64_t nseg, const ull* __restrict__ col,
                                                              const SegTot* seg_off, uint32_t* flist, ull* rowoff,
@@ -222,10 +228,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   uint64_t k = o.cs;  // next short list position
   ull e = o.ss;       // next short edge position
   uint64_t a = o.na;  // next long-tile position
+  uint64_t h = o.nh;  // next hub slot
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
-  unsigned nlongcols = 0;
   const unsigned lt = lanemask_lt();
-  auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt) {
+  unsigned nlongcols = 0;
+  auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt, uint64_t hub) {
     if (nt <= 8) {
       for (unsigned q = 0; q < nt; ++q) {
         const ull pos = c0 + ((ull)q << tile_shift);
@@ -233,9 +240,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
       }
     } else {  // hub column: its tiles are written by k_tile_fill
-      const ull slot = atomicAdd(&info->nlong, 1ull);
-      longlist[2 * slot] = make_uint4((uint32_t)pa, nt, (uint32_t)u, (uint32_t)(pa >> 32));
-      longlist[2 * slot + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
+      longlist[2 * hub] = make_uint4((uint32_t)pa, nt, (uint32_t)u, (uint32_t)(pa >> 32));
+      longlist[2 * hub + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
     }
   };
   for (uint64_t wb = w0; wb < w1; wb += 32) {
@@ -243,54 +249,65 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
     const uint32_t x = (w < w1) ? __ldg(bm + w) : 0u;
     const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
     if (nbits >= 96) {
-      // dense chunk: word by word, lane b handles bit b (coalesced col reads and list writes)
       unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
       while (nz) {
-        const int jw = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw);
-        const uint64_t u = (wb + jw) * 32 + lane;
-        ull c0 = 0, d = 0;
-        if ((xw >> lane) & 1u) {
-          c0 = __ldg(col + u);
-          d = __ldg(col + u + 1) - c0;
-        }
-        const bool isl = d >= half;
-        const unsigned ds = isl ? 0u : (unsigned)d;  // short degree < TILE/2
-        const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
-        const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
-        unsigned inc = ds, ia = na;  // inclusive warp scans
+        int jwb[4];
+        ull c0b[4], c1b[4];
 #pragma unroll
-        for (int s2 = 1; s2 < 32; s2 <<= 1) {
-          const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
-          const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
-          if (lane >= s2) {
-            inc += y1;
-            ia += y2;
+        for (int b = 0; b < 4; ++b) {  // col loads of 4 non-zero words in flight together
+          const int jw = nz ? __ffs(nz) - 1 : -1;
+          nz &= nz ? nz - 1 : 0u;
+          jwb[b] = jw;
+          const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
+          const bool bit = jw >= 0 && ((xw >> lane) & 1u);
+          const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
+          c0b[b] = bit ? __ldg(col + u) : 0ull;
+          c1b[b] = bit ? __ldg(col + u + 1) : 0ull;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (jwb[b] < 0) break;  // warp-uniform
+          const uint64_t u = (wb + jwb[b]) * 32 + lane;
+          const ull c0 = c0b[b], d = c1b[b] - c0b[b];
+          const bool isl = d >= half;
+          const unsigned ds = isl ? 0u : (unsigned)d;  // short degree < TILE/2
+          const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
+          const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
+          const unsigned hmask = __ballot_sync(0xFFFFFFFFu, na > 8);
+          unsigned inc = ds, ia = na;  // inclusive warp scans
+#pragma unroll
+          for (int s2 = 1; s2 < 32; s2 <<= 1) {
+            const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
+            const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
+            if (lane >= s2) {
+              inc += y1;
+              ia += y2;
+            }
           }
+          if (ds) {
+            const uint64_t pos = k + __popc(smask & lt);
+            const ull eb = e + inc - ds;
+            flist[pos] = (uint32_t)u;
+            rowoff[pos] = c0;
+            cumul[pos] = eb;
+            for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
+          }
+          if (isl) {
+            emit_long(u, c0, d, a + ia - na, na, h + __popc(hmask & lt));
+            ++nlongcols;
+          }
+          k += __popc(smask);
+          h += __popc(hmask);
+          e += __shfl_sync(0xFFFFFFFFu, inc, 31);
+          a += __shfl_sync(0xFFFFFFFFu, ia, 31);
         }
-        if (ds) {
-          const uint64_t pos = k + __popc(smask & lt);
-          const ull eb = e + inc - ds;
-          flist[pos] = (uint32_t)u;
-          rowoff[pos] = c0;
-          cumul[pos] = eb;
-          for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
-        }
-        if (isl) {
-          emit_long(u, c0, d, a + ia - na, na);
-          ++nlongcols;
-        }
-        k += __popc(smask);
-        e += __shfl_sync(0xFFFFFFFFu, inc, 31);
-        a += __shfl_sync(0xFFFFFFFFu, ia, 31);
       }
       continue;
     }
-    // lane totals of its word
-    unsigned cs = 0, na = 0;
+    // sparse chunk: lane totals of its word (4 set bits at a time)
+    unsigned cs = 0, na = 0, nh = 0;
     ull ss = 0;
-    for (uint32_t y = x; y;) {  // 4 set bits at a time
+    for (uint32_t y = x; y;) {
       ull dd[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -302,66 +319,60 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const ull d = dd[q];
-        if (d >= half) na += (unsigned)((d + tm) >> tile_shift);
-        else if (d) {
+        if (d >= half) {
+          const unsigned nt = (unsigned)((d + tm) >> tile_shift);
+          na += nt;
+          nh += nt > 8 ? 1u : 0u;
+        } else if (d) {
           cs += 1u;
           ss += d;
         }
       }
     }
     // warp exclusive scans of the lane totals
-    unsigned ics = cs, ina = na;
+    unsigned ics = cs, ina = na, inh = nh;
     ull iss = ss;
 #pragma unroll
     for (int s2 = 1; s2 < 32; s2 <<= 1) {
       const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, ics, s2);
       const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ina, s2);
+      const unsigned y4 = __shfl_up_sync(0xFFFFFFFFu, inh, s2);
       const ull y3 = __shfl_up_sync(0xFFFFFFFFu, iss, s2);
       if (lane >= s2) {
         ics += y1;
         ina += y2;
+        inh += y4;
         iss += y3;
       }
     }
     uint64_t kk = k + ics - cs;
     ull ee = e + iss - ss;
     uint64_t aa = a + ina - na;
+    uint64_t hh = h + inh - nh;
     for (uint32_t y = x; y;) {
-      int bq[4];
-      ull cq[4], dq[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // 4 set bits at a time: loads in flight together
-        const int b = y ? __ffs(y) - 1 : -1;
-        y &= y ? y - 1 : 0u;
-        bq[q] = b;
-        const uint64_t u = w * 32 + (b < 0 ? 0 : b);
-        cq[q] = b < 0 ? 0ull : __ldg(col + u);
-        dq[q] = b < 0 ? 0ull : __ldg(col + u + 1) - cq[q];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-      if (bq[q] < 0) break;
-      const uint64_t u = w * 32 + bq[q];
-      const ull c0 = cq[q], d = dq[q];
+      const int b = __ffs(y) - 1;
+      y &= y - 1;
+      const uint64_t u = w * 32 + b;
+      const ull c0 = __ldg(col + u), d = __ldg(col + u + 1) - c0;
       if (d >= half) {
         const unsigned nt = (unsigned)((d + tm) >> tile_shift);
-        emit_long(u, c0, d, aa, nt);
+        emit_long(u, c0, d, aa, nt, hh);
         aa += nt;
+        hh += nt > 8 ? 1u : 0u;
         ++nlongcols;
       } else if (d) {
         flist[kk] = (uint32_t)u;
         rowoff[kk] = c0;
         cumul[kk] = ee;
-        // a short column spans at most two tiles
         for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) tile_k[t] = (uint32_t)kk;
         ++kk;
         ee += d;
-      }
       }
     }
     k += __shfl_sync(0xFFFFFFFFu, ics, 31);
     e += __shfl_sync(0xFFFFFFFFu, iss, 31);
     a += __shfl_sync(0xFFFFFFFFu, ina, 31);
+    h += __shfl_sync(0xFFFFFFFFu, inh, 31);
   }
 #pragma unroll
   for (int s2 = 16; s2; s2 >>= 1) nlongcols += __shfl_xor_sync(0xFFFFFFFFu, nlongcols, s2);
@@ -394,7 +405,7 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   SegTot* so = static_cast<SegTot*>(rk.seg_off);
   k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
   // exclusive scan over nseg+1 segment totals (st[nseg] stays zero) -> so[nseg] = level total
-  cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0ull, 0ull},
+  cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0u, 0u, 0ull, 0ull},
                                  (uint64_t)nseg + 1, s);
   static ull p2_factor = 0;
   if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 32)
