@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _build
 
-_LIB = _build.LIB
+_LIB = os.environ.get("BFS200_LIB") or _build.LIB  # BFS200_LIB: an alternative build of the same ABI (A/B runs)
 
 BFS_OK, BFS_EINVAL, BFS_ERANGE, BFS_ENOMEM, BFS_ECUDA, BFS_ENCCL, BFS_ESTATE = 0, -1, -2, -3, -4, -5, -6
 

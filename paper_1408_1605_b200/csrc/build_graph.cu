@@ -34,10 +34,12 @@ struct PartMap {
     const int j = (int)(u / ncols);
     return j * R + i;
   }
-  // CSC sort key: relabeled local column, then ORIGINAL local row
+  // CSC sort key: relabeled local column, then relabeled local row (so each column lists its
+  // rows hot prefix first; the expansion skips warp groups that are all hot and visited)
   __device__ __forceinline__ ull key(uint64_t u, uint64_t v, const uint32_t* fwd) const {
     const uint64_t lc = (uint64_t)fwd[u] % ncols;
-    const uint64_t lr = (v / block / (uint64_t)R) * block + v % block;
+    const uint64_t vb = v / block;
+    const uint64_t lr = (vb / (uint64_t)R) * block + (fwd[v] - vb * block);
     return ((ull)lc << rbits) | (ull)lr;
   }
 };
@@ -131,30 +133,21 @@ __global__ void k_apply_moves(const uint32_t* moves, uint64_t nmoves, uint32_t* 
 }
 
 // ---- CSC / CSR assembly
-// row[t] = relabeled local row of the ORIGINAL local row in the key's low bits
-__global__ void k_keys_to_rows(const ull* keys, uint64_t n, int rbits, uint64_t block, int R, int i,
-                               const uint32_t* fwd, uint32_t* row) {
+// row[t] = the key's relabeled local row
+__global__ void k_keys_to_rows(const ull* keys, uint64_t n, int rbits, uint32_t* row) {
   const ull rmask = (1ull << rbits) - 1;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t lr = keys[t] & rmask;
-    const uint64_t m = lr / block;
-    const uint64_t vb = (m * R + i) * block;  // first global id of the row's vertex block
-    row[t] = (uint32_t)(m * block + (fwd[vb + lr % block] - vb));
-  }
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    row[t] = (uint32_t)(keys[t] & rmask);
 }
 
-// CSC key (col' << rbits | orig row) -> CSR key (row' << cbits | orig col)
-__global__ void k_csr_keys(ull* keys, uint64_t n, int rbits, int cbits, uint64_t block, int R, int i, uint64_t cbase,
-                           const uint32_t* fwd, const uint32_t* inv) {
+// CSC key (col' << rbits | row') -> CSR key (row' << cbits | orig col)
+__global__ void k_csr_keys(ull* keys, uint64_t n, int rbits, int cbits, uint64_t cbase, const uint32_t* inv) {
   const ull rmask = (1ull << rbits) - 1;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
     const ull k = keys[t];
     const uint64_t lr = k & rmask, lc = k >> rbits;
-    const uint64_t m = lr / block;
-    const uint64_t vb = (m * R + i) * block;
-    const uint64_t lr2 = m * block + (fwd[vb + lr % block] - vb);
     const uint64_t lc_orig = inv[cbase + lc] - cbase;
-    keys[t] = ((ull)lr2 << cbits) | (ull)lc_orig;
+    keys[t] = ((ull)lr << cbits) | (ull)lc_orig;
   }
 }
 
@@ -291,7 +284,7 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   rc = G_alloc(G, (void**)&rk.col, (g.ncols() + 1) * sizeof(ull));
   if (rc) return rc;
   if (rk.nnz) {
-    k_keys_to_rows<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, g.block, g.R, rk.i, fwd, rk.row);
+    k_keys_to_rows<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, rk.row);
     CKR(cudaGetLastError());
   }
   const uint64_t nc = g.ncols() + 1;
@@ -299,20 +292,14 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
   // CSR of the same local matrix for the parent pass (rows scanned in ascending ORIGINAL
-  // column order).  With a 1x1 grid the matrix is the symmetric adjacency and its CSC (rows in
-  // ascending original order) already is that CSR.
-  if (g.R * g.C == 1) {
-    rk.csr_ptr = rk.col;
-    rk.csr_col = rk.row;
-    return BFS_OK;
-  }
+  // column order; the CSC lists rows in relabeled order, so even a 1x1 grid needs its own copy)
   const uint64_t cbase = (uint64_t)rk.j * g.ncols();
   rc = G_alloc(G, (void**)&rk.csr_col, (rk.nnz ? rk.nnz : 1) * sizeof(uint32_t));
   if (rc) return rc;
   rc = G_alloc(G, (void**)&rk.csr_ptr, (g.nrows() + 1) * sizeof(ull));
   if (rc) return rc;
   if (rk.nnz) {
-    k_csr_keys<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, cbits, g.block, g.R, rk.i, cbase, fwd, inv);
+    k_csr_keys<<<4096, 256, 0, s>>>(keys, rk.nnz, rbits, cbits, cbase, inv);
     CKR(cudaGetLastError());
     tmp_bytes = 0;
     CKR(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys, (uint64_t)rk.nnz, 0, rbits + cbits, s));
