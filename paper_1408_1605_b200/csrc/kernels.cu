@@ -21,6 +21,8 @@
 
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace bfs200 {
@@ -54,6 +56,16 @@ __device__ __forceinline__ void ld_stream_u32_if(bool p, const uint32_t* a, uint
 __device__ __forceinline__ void ld_cg_u2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
   asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
                : "+r"(x), "+r"(y) : "l"(a), "r"((int)p));
+}
+// predicated loads whose destinations are undefined when the predicate is false (no register
+// initialisation; every use is guarded by the same predicate)
+__device__ __forceinline__ void ld_stream_u32_p(bool p, const uint32_t* a, uint32_t& v) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
+      : "=r"(v) : "l"(a), "r"((int)p));
+}
+__device__ __forceinline__ void ld_cg_u2_p(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
+      : "=r"(x), "=r"(y) : "l"(a), "r"((int)p));
 }
 __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q red.relaxed.gpu.global.or.b32 [%0], %1; }"
@@ -191,7 +203,7 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   info->newv = 0;
   // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
   // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-  // the scan (P2) is used when that is <= p2_factor (default 32); otherwise (small frontiers,
+  // the scan (P2) is used when that is <= p2_factor (default 8); otherwise (small frontiers,
   // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).  P2 also when
   // few rows remain to be discovered (the scans are then few, whatever their length):
   // remaining = rows with entries - rows discovered so far (an estimate on this rank).
@@ -408,9 +420,9 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0u, 0u, 0ull, 0ull},
                                  (uint64_t)nseg + 1, s);
   static ull p2_factor = 0;
-  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 32)
+  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 8)
     const char* env = getenv("BFS200_P2_FACTOR");
-    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 32ull;
+    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 8ull;
   }
   k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
@@ -433,40 +445,117 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 // parent's global id.
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
-constexpr size_t kHotSmem = 96 * 1024;
+constexpr size_t kSmemTarget = 160 * 1024;  // K1 dynamic shared memory (staging + hot copy)
+
+// Visited word of row v in the shared-memory hot copy.  Layout: per row segment hw words of the
+// hot prefix and one zero sentinel (word hw), so rows past the prefix need no range test: their
+// lookup lands on the sentinel and they take the L2 probe.
+template <bool SEG1>
+__device__ __forceinline__ uint32_t hot_word(const uint32_t* s_hot, uint32_t v, bool ok, uint32_t hw, int bl,
+                                             uint32_t bmask) {
+  if (SEG1) return s_hot[min(v >> 5, hw)];  // one segment: v is the offset (any v stays in bounds)
+  const uint32_t idx = (v >> bl) * (hw + 1) + min((v & bmask) >> 5, hw);
+  return s_hot[ok ? idx : hw];
+}
+
+// Visited test of one row of a P2 level, hand-scheduled (the hot loop of K1): probe the hot copy
+// (32-bit shared address sa, SEG1 layout: hw words + sentinel), then, if the row is neither hot
+// and visited nor invalid (pos >= len), one 8-byte L2 load of its visited|discovered pair.
+// Outputs: need (0/1), the bit mask m, the pair x|y and the pair's address for the RED.
+#ifndef BFS200_PROBE_LD
+#define BFS200_PROBE_LD "ld.global.cg.v2.u32"
+#endif
+struct Probe {
+  uint32_t x, y, need, m;
+  uint32_t* a;
+};
+__device__ __forceinline__ void probe_seg1(Probe& p, uint32_t v, uint32_t pos, uint32_t len, uint32_t hw, uint32_t sa,
+                                           uint32_t* vd) {
+  asm("{\n"
+      " .reg .pred pok, pn;\n"
+      " .reg .b32 wi, hi, hv;\n"
+      " setp.lt.u32 pok, %6, %7;\n"
+      " shr.b32 wi, %5, 5;\n"
+      " min.u32 hi, wi, %8;\n"
+      " shl.b32 hi, hi, 2;\n"
+      " add.u32 hi, hi, %9;\n"
+      " ld.shared.u32 hv, [hi];\n"
+      " shf.l.wrap.b32 %3, 0, 1, %5;\n"
+      " and.b32 hv, hv, %3;\n"
+      " setp.eq.and.b32 pn, hv, 0, pok;\n"
+      " mad.wide.u32 %4, wi, 8, %10;\n"
+      " @pn " BFS200_PROBE_LD " {%0, %1}, [%4];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
+      "}"
+      : "=r"(p.x), "=r"(p.y), "=r"(p.need), "=r"(p.m), "=l"(p.a)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
+}
+// general layout (C row segments of hw words + sentinel each)
+__device__ __forceinline__ void probe_segs(Probe& p, uint32_t v, uint32_t pos, uint32_t len, uint32_t hw, uint32_t sa,
+                                           uint32_t* vd, int bl, uint32_t bmask) {
+  asm("{\n"
+      " .reg .pred pok, pn;\n"
+      " .reg .b32 wi, hi, hv, sg, off;\n"
+      " setp.lt.u32 pok, %6, %7;\n"
+      " shr.b32 wi, %5, 5;\n"
+      " shr.b32 sg, %5, %11;\n"
+      " and.b32 off, %5, %12;\n"
+      " shr.b32 off, off, 5;\n"
+      " min.u32 off, off, %8;\n"
+      " add.u32 hv, %8, 1;\n"
+      " mad.lo.u32 hi, sg, hv, off;\n"
+      " selp.u32 hi, hi, %8, pok;\n"
+      " shl.b32 hi, hi, 2;\n"
+      " add.u32 hi, hi, %9;\n"
+      " ld.shared.u32 hv, [hi];\n"
+      " shf.l.wrap.b32 %3, 0, 1, %5;\n"
+      " and.b32 hv, hv, %3;\n"
+      " setp.eq.and.b32 pn, hv, 0, pok;\n"
+      " mad.wide.u32 %4, wi, 8, %10;\n"
+      " @pn " BFS200_PROBE_LD " {%0, %1}, [%4];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
+      "}"
+      : "=r"(p.x), "=r"(p.y), "=r"(p.need), "=r"(p.m), "=l"(p.a)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+}
+// RED.OR of the discovered bit if the probe was needed and neither bit is set (Alg.3 line 7)
+__device__ __forceinline__ void probe_red(const Probe& p) {
+  asm volatile("{\n"
+               " .reg .pred pn, pr;\n"
+               " .reg .b32 t;\n"
+               " setp.ne.b32 pn, %3, 0;\n"
+               " lop3.b32 t, %0, %1, %2, 0xa8;\n"
+               " setp.eq.and.b32 pr, t, 0, pn;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [%4+4], %2;\n"
+               "}" ::"r"(p.x), "r"(p.y), "r"(p.m), "r"(p.need), "l"(p.a));
+}
 
 // One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
 // against the shared-memory copy, the others with one 8-byte load of the visited|discovered
 // pair), then the discovered bit by RED.OR and, in P1 levels, the parent claim.
-template <int WV, bool P1>
+template <int WV, bool P1, bool SEG1>
 __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vd,
-                                             uint32_t* pmin, const uint32_t* s_hot, uint32_t hot_bits,
-                                             uint32_t bmask, int blog, uint32_t hw) {
+                                             uint32_t* pmin, const uint32_t* s_hot, uint32_t bmask, int bl,
+                                             uint32_t hw) {
   uint32_t wx[WV], wy[WV];
+  bool need[WV];
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
     const bool ok = v[q] != 0xFFFFFFFFu;
-    bool need = ok;
-    if (!P1) {
-      const uint32_t off = v[q] & bmask;
-      const bool inhot = ok && off < hot_bits;
-      const uint32_t hword = s_hot[inhot ? (v[q] >> blog) * hw + (off >> 5) : 0u];
-      need = ok && !(inhot && ((hword >> (off & 31)) & 1u));
-    }
-    wx[q] = 0xFFFFFFFFu;
-    wy[q] = 0xFFFFFFFFu;
-    ld_cg_u2_if(need, vd + 2 * (v[q] >> 5), wx[q], wy[q]);
+    need[q] = ok;
+    if (!P1) need[q] = ok && !(hot_word<SEG1>(s_hot, v[q], ok, hw, bl, bmask) & (1u << (v[q] & 31)));
+    ld_cg_u2_p(need[q], vd + 2 * (v[q] >> 5), wx[q], wy[q]);
   }
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
     const uint32_t m = 1u << (v[q] & 31);
-    const bool cand = !(wx[q] & m);  // not visited (Alg.3 lines 5-6)
+    const bool cand = need[q] && !(wx[q] & m);  // not visited (Alg.3 lines 5-6)
     if (P1 && cand) atomicMin(pmin + v[q], ug[q]);  // parent claim: minimum original id (R1)
     red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
   }
 }
 
-template <int E, int THREADS, bool P1, bool SEG1>
+template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
                                             const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
@@ -479,26 +568,33 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   constexpr int WV = E < 4 ? E : 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  ull* s_off = reinterpret_cast<ull*>(smem) + wid * SLOT;
-  uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + wid * SLOT;
+  // staged row positions: 32-bit when every CSC position fits (nnz < 2^32; modular arithmetic
+  // below stays exact), which leaves more of the SM's unified L1/shared memory to L1
+  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  Pos* s_off = reinterpret_cast<Pos*>(smem) + wid * SLOT;
+  uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + wid * SLOT;
   // the region after the staging holds either the parents' ids (P1) or the hot visited bits
-  uint32_t* s_region = reinterpret_cast<uint32_t*>(reinterpret_cast<ull*>(smem) + WARPS * SLOT) + WARPS * SLOT;
+  uint32_t* s_region = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + WARPS * SLOT;
   uint32_t* s_u = s_region + wid * SLOT;
   const uint32_t* s_hot = s_region;
   uint32_t hw = 0;
   if (!P1 && all_edges >= kHotMinEdges && blog >= 0) hw = hot_words;
-  for (uint32_t k = threadIdx.x; k < (uint32_t)C * hw; k += THREADS) {
-    const uint32_t m = k / hw, w = k - m * hw;
-    s_region[k] = vd[2 * ((uint64_t)m * W + w)];
+  if (!P1) {  // hot prefix of every row segment + its zero sentinel (hw = 0: sentinels only)
+    const uint32_t hs = hw + 1;
+    for (uint32_t k = threadIdx.x; k < (uint32_t)C * hs; k += THREADS) {
+      const uint32_t m = k / hs, w = k - m * hs;
+      s_region[k] = w < hw ? vd[2 * ((uint64_t)m * W + w)] : 0u;
+    }
   }
   __syncthreads();
-  const uint32_t hot_bits = hw * 32;
+  // 32-bit shared address of the hot copy, opaque to the compiler so it stays in a register
+  uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_hot);
+  asm volatile("" : "+r"(sa));
   const uint32_t bmask = (blog >= 0) ? ((1u << blog) - 1u) : 0u;
   const ull stride = (ull)gridDim.x * WARPS;
   // ---- long columns: column-aligned tiles, positions pos + e, no mapping work
+  const int bl = blog >= 0 ? blog : 31;  // blog < 0 (no hot copy): every row maps to sentinel 0
   {
-    const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
-    const int bl = blog > 0 ? blog : 0;
     constexpr int LWV = E <= 8 ? E : 8;  // all loads of a wave in flight together
     // Double-buffered: the next tile's row loads are issued before this tile's visited tests,
     // so each warp keeps two tiles of row data in flight (the level streams `row` from HBM).
@@ -509,8 +605,12 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       const uint32_t len = valid ? r.z : 0u;
 #pragma unroll
       for (int q = 0; q < LE; ++q) {
-        v[q] = 0xFFFFFFFFu;
-        ld_stream_u32_if(32u * q + lane < len, rp + 32 * q, v[q]);  // Alg.3 line 4
+        if (P1) {  // P1 tests validity by the id; P2 by the position
+          v[q] = 0xFFFFFFFFu;
+          ld_stream_u32_if(32u * q + lane < len, rp + 32 * q, v[q]);  // Alg.3 line 4
+        } else {
+          ld_stream_u32_p(32u * q + lane < len, rp + 32 * q, v[q]);
+        }
       }
     };
     auto process = [&](const uint4& r, const uint32_t (&v)[LE], uint32_t ug0) {
@@ -523,30 +623,16 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           uint32_t ug[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
-          expand_edges<LWV, true>(vw, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw);
         } else {
-          uint32_t x[LWV], y[LWV];
+          Probe pr[LWV];
 #pragma unroll
-          for (int q = 0; q < LWV; ++q) {
-            const bool ok = vw[q] != 0xFFFFFFFFu;
-            bool hv;
-            if (SEG1) {  // one row segment (C == 1): the row id is the offset; invalid ids are not hot
-              const uint32_t hword = s_hot[min(vw[q], hclamp) >> 5];
-              hv = vw[q] < hot_bits && ((hword >> (vw[q] & 31)) & 1u);
-            } else {
-              const uint32_t off = vw[q] & bmask;
-              const uint32_t hword = s_hot[ok ? (vw[q] >> bl) * hw + (min(off, hclamp) >> 5) : 0u];
-              hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
-            }
-            x[q] = 0xFFFFFFFFu;
-            y[q] = 0xFFFFFFFFu;
-            ld_cg_u2_if(ok && !hv, vd + 2 * (vw[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
+          for (int q = 0; q < LWV; ++q) {  // Alg.3 lines 5-6
+            if (SEG1) probe_seg1(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vd);
+            else probe_segs(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vd, bl, bmask);
           }
 #pragma unroll
-          for (int q = 0; q < LWV; ++q) {
-            const uint32_t m = 1u << (vw[q] & 31);
-            red_or_if(!((x[q] | y[q]) & m), vd + 2 * (vw[q] >> 5) + 1, m);  // Alg.3 line 7
-          }
+          for (int q = 0; q < LWV; ++q) probe_red(pr[q]);
         }
       }
     };
@@ -612,14 +698,14 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     if (lane < cnt) {
       const uint32_t beg = rc > t0 ? (uint32_t)(rc - t0) : 0u;
       s_beg[lane] = beg;
-      s_off[lane] = ro + (t0 + beg - rc);
+      s_off[lane] = (Pos)(ro + (t0 + beg - rc));
       if (P1) s_u[lane] = ru;
     }
     for (uint32_t idx = 32 + lane; idx < cnt; idx += 32) {  // tiles of many short columns
       const ull c = cumul[klo + idx];
       const uint32_t beg = c > t0 ? (uint32_t)(c - t0) : 0u;
       s_beg[idx] = beg;
-      s_off[idx] = rowoff[klo + idx] + (t0 + beg - c);
+      s_off[idx] = (Pos)(rowoff[klo + idx] + (t0 + beg - c));
       if (P1) s_u[idx] = inv_col[flist[klo + idx]];
     }
     if (lane == 0) s_beg[cnt] = 0xFFFFFFFFu;
@@ -644,8 +730,6 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       // lean path (the bulk of a dense level): a full tile inside one column, positions base + e,
       // every lane valid; branch-free visited test, predicated probe and RED.
       const uint32_t* rp = row + s_off[0] + lane;
-      const uint32_t hclamp = hot_bits ? hot_bits - 1 : 0u;
-      const int bl = blog > 0 ? blog : 0;
       constexpr int LWV = E <= 8 ? E : 8;  // all loads of the wave in flight together
 #pragma unroll
       for (int wv = 0; wv < E / LWV; ++wv) {
@@ -653,25 +737,18 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
 #pragma unroll
         for (int q = 0; q < LWV; ++q) v[q] = ld_stream_u32(rp + 32 * (LWV * wv + q));  // Alg.3 line 4
         if (wv == 0) prefetch_next();
-        uint32_t x[LWV], y[LWV];
+        Probe pr[LWV];
 #pragma unroll
-        for (int q = 0; q < LWV; ++q) {
-          const uint32_t off = v[q] & bmask;
-          const uint32_t hword = s_hot[(v[q] >> bl) * hw + (min(off, hclamp) >> 5)];
-          const bool hv = (off < hot_bits) && ((hword >> (off & 31)) & 1u);
-          x[q] = 0xFFFFFFFFu;
-          y[q] = 0xFFFFFFFFu;
-          ld_cg_u2_if(!hv, vd + 2 * (v[q] >> 5), x[q], y[q]);  // Alg.3 lines 5-6
+        for (int q = 0; q < LWV; ++q) {  // Alg.3 lines 5-6
+          if (SEG1) probe_seg1(pr[q], v[q], 0u, 1u, hw, sa, vd);
+          else probe_segs(pr[q], v[q], 0u, 1u, hw, sa, vd, bl, bmask);
         }
 #pragma unroll
-        for (int q = 0; q < LWV; ++q) {
-          const uint32_t m = 1u << (v[q] & 31);
-          red_or_if(!((x[q] | y[q]) & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
-        }
+        for (int q = 0; q < LWV; ++q) probe_red(pr[q]);
       }
     } else if (cnt == 1) {
       // the whole tile lies in one column: positions are base + e, no mapping work
-      const ull base = s_off[0];
+      const Pos base = s_off[0];
       const uint32_t u0 = P1 ? s_u[0] : 0u;
 #pragma unroll
       for (int wv = 0; wv < E / WV; ++wv) {
@@ -680,11 +757,11 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         for (int q = 0; q < WV; ++q) {
           const uint32_t e = 32u * (WV * wv + q) + lane;
           v[q] = 0xFFFFFFFFu;
-          ld_stream_u32_if(e < len, row + base + e, v[q]);  // Alg.3 line 4
+          ld_stream_u32_if(e < len, row + (Pos)(base + e), v[q]);  // Alg.3 line 4
           ug[q] = u0;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw);
       }
     } else {
       // lane-interleaved edges e = 32q + lane; lane state: the staged column idx holding its
@@ -701,7 +778,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         idx = (uint32_t)lane >= s_beg[1] ? 1u : 0u;
       }
       uint32_t cur_end = s_beg[idx + 1];
-      ull base = s_off[idx] - s_beg[idx];
+      Pos base = s_off[idx] - s_beg[idx];
 #pragma unroll
       for (int wv = 0; wv < E / WV; ++wv) {
         uint32_t v[WV], ug[WV];
@@ -713,7 +790,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
             const bool adv = ok && e >= cur_end;
             idx += adv ? 1u : 0u;
             const uint32_t nb = s_beg[idx], ne = s_beg[idx + 1];
-            const ull no = s_off[idx];
+            const Pos no = s_off[idx];
             if (adv) {
               cur_end = ne;
               base = no - nb;
@@ -727,11 +804,11 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
             }
           }
           v[q] = 0xFFFFFFFFu;
-          ld_stream_u32_if(ok, row + base + e, v[q]);  // Alg.3 line 4
+          ld_stream_u32_if(ok, row + (Pos)(base + e), v[q]);  // Alg.3 line 4 (modular when Pos is 32-bit)
           ug[q] = P1 ? s_u[idx] : 0u;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1>(v, ug, vd, pmin, s_hot, hot_bits, bmask, blog, hw);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw);
       }
     }
     if (!rnext) {
@@ -745,7 +822,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   }
 }
 
-template <int E, int THREADS, bool SEG1>
+template <int E, int THREADS, bool SEG1, bool POS32>
 __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
                                                        const uint32_t* __restrict__ flist,
                                                        const ull* __restrict__ rowoff,
@@ -758,10 +835,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
   const ull n = info->n, total = info->sedges, nA = info->nA, all_edges = info->edges;
   if (all_edges == 0) return;
   if (info->mode == 1)
-    expand_body<E, THREADS, true, SEG1>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+    expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
                                   inv_col, hot_words, C, W, blog);
   else
-    expand_body<E, THREADS, false, SEG1>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
+    expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
                                    inv_col, hot_words, C, W, blog);
 }
 
@@ -769,7 +846,8 @@ template <int E, int THREADS>
 static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cudaStream_t s) {
   constexpr int SLOT = 32 * E + 2;
   constexpr size_t WARPS = THREADS / 32;
-  const size_t staging = WARPS * SLOT * (8 + 4);
+  const bool pos32 = rk.nnz < (1ull << 32);  // every CSC position fits in 32 bits
+  const size_t staging = WARPS * SLOT * ((pos32 ? 4 : 8) + 4);
   const size_t s_u_bytes = WARPS * SLOT * 4;
   // hot visited words per row segment: the relabeled prefix, as far as shared memory allows
   int blog = -1;
@@ -778,30 +856,35 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
     while ((1ull << blog) < g.block) ++blog;
   }
   uint64_t hw = hot_h / 32;
-  // the hot copy gets at most kHotSmem bytes: the rest of the SM's 228 KB stays L1 cache
-  static size_t hot_smem = 0;
-  if (!hot_smem) {  // tuning knob for experiments: BFS200_HOT_KB (default 128)
+  // The hot copy fills the shared memory up to kSmemTarget in all: a larger carve-out costs L1
+  // capacity, which holds the in-flight row loads and probes (measured at s26, peak level:
+  // 162 KB of shared memory 3.67 ms, 178 KB 4.28 ms, 210 KB 6.9 ms).
+  static long env_kb = -1;
+  if (env_kb < 0) {  // tuning knob for experiments: BFS200_HOT_KB (hot copy size, overrides the target)
     const char* env = getenv("BFS200_HOT_KB");
-    hot_smem = (env && atoi(env) > 0) ? (size_t)atoi(env) * 1024 : kHotSmem;
+    env_kb = (env && atoi(env) > 0) ? atoi(env) : 0;
   }
+  const size_t hot_smem = env_kb ? (size_t)env_kb * 1024
+                                 : (kSmemTarget > staging + 16 + 64 ? kSmemTarget - staging - 16 - 64 : 4);
   const uint64_t budget = hot_smem < kSmemBudget - staging - 16 ? hot_smem : kSmemBudget - staging - 16;
-  const uint64_t cap = budget / 4 / (uint64_t)g.C;
+  const uint64_t cap = budget / 4 / (uint64_t)g.C - 1;  // + one sentinel word per segment
   if (hw > cap) hw = cap;
   if (blog < 0) hw = 0;
-  size_t region = (size_t)g.C * hw * 4;
+  size_t region = (size_t)g.C * (hw + 1) * 4;
   if (region < s_u_bytes) region = s_u_bytes;
   const size_t smem = staging + region + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_expand<E, THREADS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    cudaFuncSetAttribute(k_expand<E, THREADS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaFuncSetAttribute(k_expand<E, THREADS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
     attr = true;
   }
-  auto kern = g.C == 1 ? k_expand<E, THREADS, true> : k_expand<E, THREADS, false>;
-  kern<<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA,
-                                                        rk.info,
-                                                        rk.vd, rk.pmin, rk.inv_col, (uint32_t)hw, g.C,
-                                                        g.words_block(), blog);
+  auto kern = g.C == 1 ? (pos32 ? k_expand<E, THREADS, true, true> : k_expand<E, THREADS, true, false>)
+                       : (pos32 ? k_expand<E, THREADS, false, true> : k_expand<E, THREADS, false, false>);
+  kern<<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vd,
+                                        rk.pmin, rk.inv_col, (uint32_t)hw, g.C, g.words_block(), blog);
   return cudaGetLastError();
 }
 
