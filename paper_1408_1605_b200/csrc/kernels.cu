@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   const unsigned lt = lanemask_lt();
   unsigned nlongcols = 0;
+  __shared__ uint16_t s_lists[kScanThreads / 32][1024];
+  uint16_t* s_list = s_lists[threadIdx.x >> 5];
   auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt, uint64_t hub) {
     if (nt <= 8) {
       for (unsigned q = 0; q < nt; ++q) {
@@ -261,25 +263,33 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
     const uint32_t x = (w < w1) ? __ldg(bm + w) : 0u;
     const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
     if (nbits >= 96) {
-      unsigned nz = __ballot_sync(0xFFFFFFFFu, x != 0);
-      while (nz) {
-        int jwb[4];
-        ull c0b[4], c1b[4];
+      // dense chunk: compact its set bits (column offsets in the chunk, ascending) into this
+      // warp's shared list, then emit 32 frontier columns per step with every lane busy
+      const unsigned c = __popc(x);
+      unsigned incl = c;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {  // col loads of 4 non-zero words in flight together
-          const int jw = nz ? __ffs(nz) - 1 : -1;
-          nz &= nz ? nz - 1 : 0u;
-          jwb[b] = jw;
-          const uint32_t xw = __shfl_sync(0xFFFFFFFFu, x, jw < 0 ? 0 : jw);
-          const bool bit = jw >= 0 && ((xw >> lane) & 1u);
-          const uint64_t u = (wb + (jw < 0 ? 0 : jw)) * 32 + lane;
-          c0b[b] = bit ? __ldg(col + u) : 0ull;
-          c1b[b] = bit ? __ldg(col + u + 1) : 0ull;
+      for (int s2 = 1; s2 < 32; s2 <<= 1) {
+        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, s2);
+        if (lane >= s2) incl += y;
+      }
+      unsigned p = incl - c;
+      for (uint32_t y = x; y; y &= y - 1) s_list[p++] = (uint16_t)(lane * 32 + __ffs(y) - 1);
+      __syncwarp();
+      for (unsigned g = 0; g < nbits; g += 64) {
+        ull c0b[2], c1b[2];
+        uint64_t ub[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // col loads of two groups in flight together
+          const unsigned idx = g + 32 * b + lane;
+          const bool valid = idx < nbits;
+          ub[b] = wb * 32 + (valid ? s_list[idx] : 0u);
+          c0b[b] = valid ? __ldg(col + ub[b]) : 0ull;
+          c1b[b] = valid ? __ldg(col + ub[b] + 1) : 0ull;
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (jwb[b] < 0) break;  // warp-uniform
-          const uint64_t u = (wb + jwb[b]) * 32 + lane;
+        for (int b = 0; b < 2; ++b) {
+          if (g + 32 * b >= nbits) break;  // warp-uniform
+          const uint64_t u = ub[b];
           const ull c0 = c0b[b], d = c1b[b] - c0b[b];
           const bool isl = d >= half;
           const unsigned ds = isl ? 0u : (unsigned)d;  // short degree < TILE/2
@@ -314,6 +324,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
           a += __shfl_sync(0xFFFFFFFFu, ia, 31);
         }
       }
+      __syncwarp();  // the list is rewritten by the next chunk
       continue;
     }
     // sparse chunk: lane totals of its word (4 set bits at a time)
