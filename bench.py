@@ -162,8 +162,17 @@ def sample_roots_collective(n, count, degree):
     return roots
 
 
+def grid_of(args, world):
+    if args.grid:
+        R, C = (int(x) for x in args.grid.lower().split("x"))
+        if R * C != world:
+            raise SystemExit(f"--grid {args.grid} needs {R * C} ranks, have {world}")
+        return R, C
+    return GRIDS.get(world, (1, world))
+
+
 def workload_config(args, world):
-    R, C = GRIDS.get(world, (1, world))
+    R, C = grid_of(args, world)
     scale = args.scale if args.scale else 26 + int(round(math.log2(world)))
     return {"workload": f"graph500-kronecker-s{scale}-ef16-{R}x{C}", "scale": scale, "edgefactor": 16,
             "grid": f"{R}x{C}", "roots": 64, "parallelism": f"2d-{R}x{C}", "edges_per_thread": args.E,
@@ -180,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     cfg = workload_config(args, world)
     scale = cfg["scale"]
-    R, C = GRIDS.get(world, (1, world))
+    R, C = grid_of(args, world)
     n = 1 << scale
     M = inputs.num_tuples(scale)
     # this rank's slice of the tuple list, generated in HBM
@@ -278,9 +287,10 @@ def run_ours(args, rank, world, local_rank):
                 exp_ms += rec.expand
         g.set_opts(opts)
 
-    # e2e: same metric through the C ABI with HOST output buffers (D2H inside the timed region)
+    # e2e: same metric through the C ABI with a HOST output buffer (D2H inside the timed region).
+    # The result read back is the BFS tree (parent array, Graph500's output); levels are optional
+    # in the API and not requested here.
     ph = torch.empty(info.nout, dtype=torch.int64).pin_memory()
-    lh = torch.empty(info.nout, dtype=torch.int32).pin_memory()
     e2e_teps = []
     for k in range(args.steps):
         r = timed_roots[k % len(timed_roots)]
@@ -288,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        g.run(r, ph, lh)  # returns after the host buffers are complete
+        g.run(r, ph)  # returns after the host buffer is complete
         t_s = max_over_ranks(time.perf_counter() - t0)
         e2e_teps.append(mcomps[k % len(mcomps)] / t_s)
     e2e = hmean(e2e_teps) / 1e9
@@ -314,7 +324,7 @@ def run_ours(args, rank, world, local_rank):
                                                      "root seed 2)",
         "config": cfg,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8,
-                "d2h_bytes_per_step": int(info.nout) * 12 * world},
+                "d2h_bytes_per_step": int(info.nout) * 8 * world, "result": "parent array (int64 per vertex)"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
@@ -347,6 +357,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--E", type=int, default=4)
+    ap.add_argument("--grid", default="", help="RxC override of the default grid (1x1, 1x2, 2x2, 2x4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase-timing", action="store_true", help="(diagnostic) no per-phase events")
     args = ap.parse_args()
