@@ -1085,36 +1085,52 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
   // grid: x over the words of one segment, y = segment m (no 64-bit division)
   const int lvl = (int)ctrl->lvl;  // the level being assigned (device-side: the loop may be a graph)
   const int m = (int)blockIdx.y;
+  const int lane = threadIdx.x & 31;
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t gid = (uint64_t)m * W + w;
   uint32_t newbits = 0;
-  if (w < W) {
-    uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
-    if (m != j) {
-      if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
-    } else {
-      const uint32_t vis = p.x;
-      uint32_t claimed = 0;
-      for (int c = 0; c < C; ++c) {
-        const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
-        if (x && winner) {
-          uint32_t b = x;
-          while (b) {
-            const int bit = __ffs(b) - 1;
-            b &= b - 1;
-            winner[w * 32 + bit] = (uint8_t)c;
-          }
+  uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
+  if (m == j && w < W) {
+    const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
+    const uint32_t vis = p.x;
+    uint32_t claimed = 0;
+    for (int c = 0; c < C; ++c) {
+      const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
+      if (c < 8) wbits[c] = x;
+      if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
+        uint32_t b = x;
+        while (b) {
+          const int bit = __ffs(b) - 1;
+          b &= b - 1;
+          winner[w * 32 + bit] = (uint8_t)c;
         }
-        claimed |= x;
       }
-      newbits = claimed;
-      if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
-      front_seg[w] = newbits;
-      uint32_t b = newbits;
-      while (b) {
-        const int bit = __ffs(b) - 1;
-        b &= b - 1;
-        level[w * 32 + bit] = lvl;
+      claimed |= x;
+    }
+    newbits = claimed;
+    if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
+    front_seg[w] = newbits;
+  } else if (w < W) {
+    const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
+    if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
+  }
+  // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing vertex
+  // 32k + l of word k (coalesced stores instead of per-bit scattered ones)
+  if (m == j) {
+    const uint64_t wbase = w - lane;
+    unsigned nz = __ballot_sync(0xFFFFFFFFu, newbits != 0);
+    while (nz) {
+      const int k = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t nb = __shfl_sync(0xFFFFFFFFu, newbits, k);
+      const uint64_t v = (wbase + k) * 32 + lane;
+      if ((nb >> lane) & 1u) level[v] = lvl;
+      if (winner) {
+        const int cmax = C < 8 ? C : 8;
+        for (int c = 0; c < cmax; ++c) {
+          const uint32_t x = __shfl_sync(0xFFFFFFFFu, wbits[c], k);
+          if ((x >> lane) & 1u) winner[v] = (uint8_t)c;
+        }
       }
     }
   }
