@@ -26,7 +26,8 @@ struct LevelInfo {
   unsigned long long edges;   // all CSC entries leaving the frontier (short + long)
   unsigned long long newv;    // vertices discovered by the update (this rank)
   unsigned long long mode;    // parent claim of this level: 1 = atomicMin in the expansion (P1),
-                              // 2 = CSR scan of the discovered rows (P2); see k_scan_segs
+                              // 2 = CSR scan of the discovered rows (P2), 3 = P1 with the
+                              // discovered words derived from pmin; see k_level_info
   unsigned long long nlong;   // hub columns whose long-tile records are written by k_tile_fill
   unsigned long long sedges;  // edges of the short columns = cumul[n]
   unsigned long long nA;      // long-column tiles (tileA records)

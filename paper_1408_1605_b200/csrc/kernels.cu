@@ -154,8 +154,50 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   SegTot t{0u, 0u, 0ull, 0ull};
-  for (uint64_t w = w0 + lane; w < w1; w += 32) {
-    uint32_t x = __ldg(bm + w);
+  __shared__ uint16_t s_lists[kScanThreads / 32][1024];
+  uint16_t* s_list = s_lists[threadIdx.x >> 5];
+  auto add_col = [&](ull d) {
+    if (d >= half) {
+      const unsigned nt = (unsigned)((d + tm) >> tile_shift);
+      t.na += nt;
+      t.nh += nt > 8 ? 1u : 0u;
+      t.ls += d;
+    } else if (d) {
+      t.cs += 1u;
+      t.ss += d;
+    }
+  };
+  for (uint64_t wb = w0; wb < w1; wb += 32) {
+    const uint64_t w = wb + lane;
+    uint32_t x = (w < w1) ? __ldg(bm + w) : 0u;
+    const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
+    if (nbits >= 96) {
+      // dense chunk: compact the set bits, then 32 consecutive frontier columns per step (their
+      // col[] entries share lines) -- the same order as k_scan_emit
+      const unsigned c = __popc(x);
+      unsigned incl = c;
+#pragma unroll
+      for (int s2 = 1; s2 < 32; s2 <<= 1) {
+        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, s2);
+        if (lane >= s2) incl += y;
+      }
+      unsigned p = incl - c;
+      for (uint32_t y = x; y; y &= y - 1) s_list[p++] = (uint16_t)(lane * 32 + __ffs(y) - 1);
+      __syncwarp();
+      for (unsigned g = 0; g < nbits; g += 64) {
+        ull dd[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const unsigned idx = g + 32 * b + lane;
+          const uint64_t u = wb * 32 + (idx < nbits ? s_list[idx] : 0u);
+          dd[b] = idx < nbits ? __ldg(col + u + 1) - __ldg(col + u) : 0ull;
+        }
+        add_col(dd[0]);
+        add_col(dd[1]);
+      }
+      __syncwarp();
+      continue;
+    }
     while (x) {  // 4 set bits at a time: their col[] loads are in flight together
       ull dd[4];
 #pragma unroll
@@ -166,18 +208,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
         dd[q] = b < 0 ? 0ull : __ldg(col + u + 1) - __ldg(col + u);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const ull d = dd[q];
-        if (d >= half) {
-          const unsigned nt = (unsigned)((d + tm) >> tile_shift);
-          t.na += nt;
-          t.nh += nt > 8 ? 1u : 0u;
-          t.ls += d;
-        } else if (d) {
-          t.cs += 1u;
-          t.ss += d;
-        }
-      }
+      for (int q = 0; q < 4; ++q) add_col(dd[q]);
     }
   }
 #pragma unroll
@@ -193,7 +224,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
 
 // level totals from the segment scan (seg_off[nseg] = sum over all segments); resets counters
 __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* info, ull* cumul, ull nnz,
-                             ull p2_factor, ull nz_rows) {
+                             ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
   const SegTot c = seg_off[nseg];
   info->n = c.cs;
   info->sedges = c.ss;
@@ -210,6 +241,10 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   const ull edges = c.ss + c.ls, seen = info->disc_total;
   const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
   info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
+  // P1 with many candidate edges (mode 3): the expansion only claims (atomicMin); the parent
+  // pass derives the discovered words from pmin in one pass over the rows (cheaper than a
+  // RED.OR and a probe per edge once edges * m3_factor >= rows)
+  if (info->mode == 1 && m3_factor && edges * m3_factor >= nrows) info->mode = 3ull;
   info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
   info->nlongcols = 0;
   cumul[c.cs] = c.ss;
@@ -435,7 +470,13 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
     const char* env = getenv("BFS200_P2_FACTOR");
     p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 8ull;
   }
-  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows);
+  static long m3_factor = -1;
+  if (m3_factor < 0) {  // tuning knob for experiments: BFS200_M3_FACTOR (0 disables mode 3; default 4)
+    const char* env = getenv("BFS200_M3_FACTOR");
+    m3_factor = env ? atol(env) : 4;
+  }
+  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows,
+                               (ull)m3_factor, (ull)g.nrows());
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
@@ -544,25 +585,34 @@ __device__ __forceinline__ void probe_red(const Probe& p) {
 // One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
 // against the shared-memory copy, the others with one 8-byte load of the visited|discovered
 // pair), then the discovered bit by RED.OR and, in P1 levels, the parent claim.
+// claim3 (P1 levels with a dense claim, mode 3): the claim alone, atomicMin of pmin; rows of the
+// hot prefix need no probe (their visited bit is exact in shared memory) and no discovered bit
+// is set here -- k_parent derives the discovered words from pmin.
 template <int WV, bool P1, bool SEG1>
 __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vd,
                                              uint32_t* pmin, const uint32_t* s_hot, uint32_t bmask, int bl,
-                                             uint32_t hw) {
+                                             uint32_t hw, bool claim3 = false) {
   uint32_t wx[WV], wy[WV];
-  bool need[WV];
+  bool need[WV], probe[WV];
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
     const bool ok = v[q] != 0xFFFFFFFFu;
+    const uint32_t m = 1u << (v[q] & 31);
     need[q] = ok;
-    if (!P1) need[q] = ok && !(hot_word<SEG1>(s_hot, v[q], ok, hw, bl, bmask) & (1u << (v[q] & 31)));
-    ld_cg_u2_p(need[q], vd + 2 * (v[q] >> 5), wx[q], wy[q]);
+    probe[q] = ok;
+    if (!P1 || claim3) {
+      need[q] = ok && !(hot_word<SEG1>(s_hot, v[q], ok, hw, bl, bmask) & m);
+      const uint32_t off = SEG1 ? v[q] : (v[q] & bmask);
+      probe[q] = need[q] && !(claim3 && off < hw * 32u);  // claim3: hot rows are decided already
+    }
+    ld_cg_u2_p(probe[q], vd + 2 * (v[q] >> 5), wx[q], wy[q]);
   }
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
     const uint32_t m = 1u << (v[q] & 31);
-    const bool cand = need[q] && !(wx[q] & m);  // not visited (Alg.3 lines 5-6)
+    const bool cand = need[q] && !(probe[q] && (wx[q] & m));  // not visited (Alg.3 lines 5-6)
     if (P1 && cand) atomicMin(pmin + v[q], ug[q]);  // parent claim: minimum original id (R1)
-    red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+    if (!claim3) red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
   }
 }
 
@@ -572,7 +622,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
                                             ull nA, ull n, ull total, ull all_edges, uint32_t* vd, uint32_t* pmin,
                                             const uint32_t* __restrict__ inv_col, uint32_t hot_words, int C,
-                                            uint64_t W, int blog) {
+                                            uint64_t W, int blog, uint32_t region_words, bool claim3) {
   constexpr int TILE = 32 * E;
   constexpr int WARPS = THREADS / 32;
   constexpr int SLOT = TILE + 2;
@@ -586,11 +636,16 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + wid * SLOT;
   // the region after the staging holds either the parents' ids (P1) or the hot visited bits
   uint32_t* s_region = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + WARPS * SLOT;
-  uint32_t* s_u = s_region + wid * SLOT;
+  // P1: the per-warp parents' ids sit at the end of the region, the hot copy (P2, mode 3) at its start
+  uint32_t* s_u = s_region + (region_words - WARPS * SLOT) + wid * SLOT;
   const uint32_t* s_hot = s_region;
   uint32_t hw = 0;
   if (!P1 && all_edges >= kHotMinEdges && blog >= 0) hw = hot_words;
-  if (!P1) {  // hot prefix of every row segment + its zero sentinel (hw = 0: sentinels only)
+  if (P1 && claim3 && blog >= 0) {  // mode 3: the hot copy shares the region with s_u
+    const uint32_t room = (region_words - WARPS * SLOT) / (uint32_t)C;
+    hw = room > 1 ? min(hot_words, room - 1) : 0u;
+  }
+  if (!P1 || claim3) {  // hot prefix of every row segment + its zero sentinel (hw = 0: sentinels only)
     const uint32_t hs = hw + 1;
     for (uint32_t k = threadIdx.x; k < (uint32_t)C * hs; k += THREADS) {
       const uint32_t m = k / hs, w = k - m * hs;
@@ -634,7 +689,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           uint32_t ug[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
-          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw);
+          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
         } else {
           Probe pr[LWV];
 #pragma unroll
@@ -772,7 +827,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = u0;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
       }
     } else {
       // lane-interleaved edges e = 32q + lane; lane state: the staged column idx holding its
@@ -819,7 +874,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = P1 ? s_u[idx] : 0u;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
       }
     }
     if (!rnext) {
@@ -842,15 +897,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
                                                        const uint4* __restrict__ tileA,
                                                        const LevelInfo* __restrict__ info, uint32_t* vd,
                                                        uint32_t* pmin, const uint32_t* __restrict__ inv_col,
-                                                       uint32_t hot_words, int C, uint64_t W, int blog) {
+                                                       uint32_t hot_words, int C, uint64_t W, int blog,
+                                                       uint32_t region_words) {
   const ull n = info->n, total = info->sedges, nA = info->nA, all_edges = info->edges;
   if (all_edges == 0) return;
-  if (info->mode == 1)
-    expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
-                                  inv_col, hot_words, C, W, blog);
+  if (info->mode != 2)
+    expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd,
+                                               pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3);
   else
-    expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd, pmin,
-                                   inv_col, hot_words, C, W, blog);
+    expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges,
+                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false);
 }
 
 template <int E, int THREADS>
@@ -882,7 +938,8 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   if (hw > cap) hw = cap;
   if (blog < 0) hw = 0;
   size_t region = (size_t)g.C * (hw + 1) * 4;
-  if (region < s_u_bytes) region = s_u_bytes;
+  // P1 levels keep s_u at the end of the region and (mode 3) at least the C sentinels before it
+  if (region < s_u_bytes + (size_t)g.C * 4) region = s_u_bytes + (size_t)g.C * 4;
   const size_t smem = staging + region + 16;
   static bool attr = false;
   if (!attr) {
@@ -895,7 +952,8 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   auto kern = g.C == 1 ? (pos32 ? k_expand<E, THREADS, true, true> : k_expand<E, THREADS, true, false>)
                        : (pos32 ? k_expand<E, THREADS, false, true> : k_expand<E, THREADS, false, false>);
   kern<<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vd,
-                                        rk.pmin, rk.inv_col, (uint32_t)hw, g.C, g.words_block(), blog);
+                                        rk.pmin, rk.inv_col, (uint32_t)hw, g.C, g.words_block(), blog,
+                                        (uint32_t)(region / 4));
   return cudaGetLastError();
 }
 
@@ -923,9 +981,13 @@ cudaError_t launch_expand(const Geom& g, Rank& rk, int E, uint64_t hot_h, cudaSt
 // discovered words are also packed contiguously as the fold message.
 constexpr int kParentThreads = 1024;
 constexpr int kShortScan = 32;
+#ifndef BFS200_LANE_STEP
+#define BFS200_LANE_STEP 4
+#endif
+constexpr int kLaneStep = BFS200_LANE_STEP;  // CSR entries per lane step (loads in flight together)
 constexpr size_t kParentHotSmem = 64 * 1024;  // hot prefix of the frontier bitmap (P2 levels)
 
-__global__ void __launch_bounds__(kParentThreads, 1) k_parent(const uint32_t* __restrict__ vd, uint64_t nwords,
+__global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint64_t nwords,
                                                                const ull* __restrict__ csr_ptr,
                                                                const uint32_t* __restrict__ csr_col,
                                                                const uint32_t* __restrict__ front, uint32_t* pred,
@@ -937,11 +999,11 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(const uint32_t* __
   uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const bool p1 = info->mode == 1;
+  const bool p1 = info->mode == 1, m3 = info->mode == 3;
   unsigned ndisc = 0;
   // P2: frontier bits of the hot (relabeled, highest-degree) column prefix of each of the R
   // column segments, so most frontier tests of the CSR scans stay in shared memory
-  const uint32_t hw = (!p1 && blog >= 0) ? hot_words : 0u;
+  const uint32_t hw = (!p1 && !m3 && blog >= 0) ? hot_words : 0u;
   for (uint32_t k = threadIdx.x; k < (uint32_t)R * hw; k += kParentThreads) {
     const uint32_t m = k / hw, w = k - m * hw;
     s_hot[k] = front[(uint64_t)m * Wc + w];
@@ -958,6 +1020,30 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(const uint32_t* __
   for (uint64_t ch = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid; ch < nchunks;
        ch += (uint64_t)gridDim.x * (kParentThreads / 32)) {
     const uint64_t w = ch * 32 + lane;
+    if (m3) {
+      // mode 3: the rows claimed in pmin are the discovered ones; lane l handles row 32k + l of
+      // the chunk's word k (coalesced), the ballot is word k's discovered bits
+      uint32_t myd = 0;
+      const int nk = (int)min((uint64_t)32, nwords - ch * 32);
+#pragma unroll 4
+      for (int k = 0; k < nk; ++k) {
+        const uint64_t r = (ch * 32 + k) * 32 + lane;
+        const uint32_t pm = pmin[r];
+        const bool f = pm != 0xFFFFFFFFu;
+        const unsigned dd = __ballot_sync(0xFFFFFFFFu, f);
+        if (f) {
+          pred[r] = pm;
+          pmin[r] = 0xFFFFFFFFu;
+        }
+        if (lane == k) myd = dd;
+      }
+      if (w < nwords) {
+        vd[2 * w + 1] = myd;
+        if (sendbuf) sendbuf[w] = myd;
+      }
+      ndisc += __popc(myd);
+      continue;
+    }
     const uint32_t d = (w < nwords) ? vd[2 * w + 1] : 0u;
     if (sendbuf && w < nwords) sendbuf[w] = d;
     ndisc += __popc(d);
@@ -997,16 +1083,16 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(const uint32_t* __
       const ull stop = min(end, beg + kShortScan);
       uint32_t best = 0xFFFFFFFFu;
       ull p = beg;
-      for (; p < stop && best == 0xFFFFFFFFu; p += 4) {
-        uint32_t u[4];
-        bool f[4];
+      for (; p < stop && best == 0xFFFFFFFFu; p += kLaneStep) {
+        uint32_t u[kLaneStep];
+        bool f[kLaneStep];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) u[k] = (p + k < stop) ? __ldg(csr_col + p + k) : 0xFFFFFFFFu;
+        for (int k = 0; k < kLaneStep; ++k) u[k] = (p + k < stop) ? __ldg(csr_col + p + k) : 0xFFFFFFFFu;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kLaneStep; ++k)
           f[k] = (u[k] != 0xFFFFFFFFu) && in_front(u[k]);
 #pragma unroll
-        for (int k = 3; k >= 0; --k)
+        for (int k = kLaneStep - 1; k >= 0; --k)
           if (f[k]) best = u[k];
       }
       if (best != 0xFFFFFFFFu) {
