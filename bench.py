@@ -163,7 +163,7 @@ def sample_roots_collective(n, count, degree):
 
 
 def grid_of(args, world):
-    if args.grid:
+    if getattr(args, "grid", ""):
         R, C = (int(x) for x in args.grid.lower().split("x"))
         if R * C != world:
             raise SystemExit(f"--grid {args.grid} needs {R * C} ranks, have {world}")

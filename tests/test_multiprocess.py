@@ -76,7 +76,7 @@ def test_weak_scaling_workloads():
     sys.path.insert(0, ROOT)
     import argparse
     import bench
-    a = argparse.Namespace(scale=0, E=4)
+    a = argparse.Namespace(scale=0, E=4, grid="")
     cfgs = {w: bench.workload_config(a, w) for w in (1, 2, 4, 8)}
     assert [cfgs[w]["scale"] for w in (1, 2, 4, 8)] == [26, 27, 28, 29]
     assert [cfgs[w]["grid"] for w in (1, 2, 4, 8)] == ["1x1", "1x2", "2x2", "2x4"]
