@@ -68,7 +68,18 @@ typedef struct {
   int phase_timing;     /* != 0: record CUDA events around every phase of every level; read
                            them afterwards with bfs_level_times (does not synchronise) */
   void* stream;         /* cudaStream_t all work is issued on; NULL -> a library-owned stream */
+  int exchange;         /* encoding of the per-level messages:
+                           0 BFS_XCHG_BITMAP: every message is the L/32-word bitmap (default; the
+                             level loop runs as one CUDA graph);
+                           1 BFS_XCHG_LIST: every message is its count n of raw local indices;
+                           2 BFS_XCHG_AUTO: per phase and level, a message is a list iff
+                             n <= T = L/32 (strict ">" for the bitmap), L = block.
+                           1 and 2 size the messages on the host each level (host-driven loop, one
+                           count exchange + device-to-host read per phase). Values are otherwise
+                           BFS_EINVAL. Results are identical in every mode. */
 } bfs_opts;
+
+enum { BFS_XCHG_BITMAP = 0, BFS_XCHG_LIST = 1, BFS_XCHG_AUTO = 2 };
 
 /* Shape of this process's part of the partition. */
 typedef struct {
@@ -91,7 +102,10 @@ typedef struct {
   uint64_t edges_scanned;    /* CSC entries expanded (sum over levels of cumul[n])         */
   uint64_t frontier_columns; /* frontier columns with local degree > 0, summed over levels  */
   uint64_t reached;          /* owned vertices reached (level >= 0)                        */
-  uint64_t bytes_exchanged;  /* bytes sent by this process's ranks over the transport      */
+  uint64_t bytes_exchanged;  /* bytes sent by this process's ranks over the transport
+                                (per-level messages; counts and the end-of-search resolution
+                                excluded)                                                    */
+  uint64_t list_messages;    /* per-level messages sent as index lists (exchange 1 / 2)     */
   uint64_t kernel_launches;  /* libbfs200 kernels launched by the call (CUB/NCCL excluded)  */
   double finalize_ms;        /* output write (phase_timing only, else 0)                   */
   double resolve_ms;         /* end-of-search parent exchange, C > 1 (phase_timing only)   */

@@ -32,7 +32,8 @@ class Comm(ctypes.Structure):
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("edges_per_thread", ctypes.c_int), ("phase_timing", ctypes.c_int), ("stream", ctypes.c_void_p)]
+    _fields_ = [("edges_per_thread", ctypes.c_int), ("phase_timing", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("exchange", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -45,7 +46,8 @@ class Info(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("nlevels", ctypes.c_int), ("edges_scanned", ctypes.c_uint64),
                 ("frontier_columns", ctypes.c_uint64), ("reached", ctypes.c_uint64),
-                ("bytes_exchanged", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("bytes_exchanged", ctypes.c_uint64), ("list_messages", ctypes.c_uint64),
+                ("kernel_launches", ctypes.c_uint64),
                 ("finalize_ms", ctypes.c_double), ("resolve_ms", ctypes.c_double)]
 
 
@@ -127,10 +129,15 @@ def make_comm(rank=0, nranks=1, device=0, loopback=True, nccl_id: bytes | None =
     return c
 
 
-def make_opts(edges_per_thread=4, phase_timing=False, stream=None) -> Opts:
+XCHG_BITMAP, XCHG_LIST, XCHG_AUTO = 0, 1, 2
+XCHG = {"bitmap": XCHG_BITMAP, "list": XCHG_LIST, "auto": XCHG_AUTO}
+
+
+def make_opts(edges_per_thread=4, phase_timing=False, stream=None, exchange="bitmap") -> Opts:
     o = Opts()
     o.edges_per_thread = int(edges_per_thread)
     o.phase_timing = 1 if phase_timing else 0
+    o.exchange = XCHG[exchange] if isinstance(exchange, str) else int(exchange)
     if stream is not None:
         o.stream = stream if isinstance(stream, int) else getattr(stream, "cuda_stream", None)
     return o

@@ -108,6 +108,13 @@ struct Rank {
   size_t scan_tmp_bytes = 0;
   uint32_t* resp = nullptr;      // [nrows] compacted responses (sent)
   uint32_t* respin = nullptr;    // [nrows] compacted responses (received)
+  // list exchange (opts.exchange != 0), allocated on first use; S = max(R, C) segments of W words
+  uint32_t* xsend = nullptr;     // [S*W] outgoing index lists, segment k at k*W
+  uint32_t* xrecv = nullptr;     // [S*W] incoming index lists
+  uint32_t* xoff = nullptr;      // [S*W] exclusive popcount scan of the segments being encoded
+  void* xtmp = nullptr;          // CUB temporary storage of that scan
+  size_t xtmp_bytes = 0;
+  unsigned long long* xcnt = nullptr;  // [64] per-segment counts (device)
   unsigned long long* scratch = nullptr;  // small reduction scratch
 };
 
@@ -149,6 +156,7 @@ struct Graph {
   int runs = 0;
   int ev_levels = 0;
   std::vector<uint64_t> lvl_frontier, lvl_edges;
+  uint64_t xbytes = 0, xlists = 0;  // list exchange: bytes sent and list messages in this run
 };
 
 }  // namespace bfs200

@@ -252,6 +252,8 @@ static int check_opts(const bfs_opts* o) {
   const int E = o->edges_per_thread;
   if (E != 0 && E != 1 && E != 2 && E != 4 && E != 8 && E != 16)
     return set_err(BFS_EINVAL, "edges_per_thread must be 1, 2, 4, 8 or 16 (got %d)", E);
+  if (o->exchange < BFS_XCHG_BITMAP || o->exchange > BFS_XCHG_AUTO)
+    return set_err(BFS_EINVAL, "exchange must be 0 (bitmap), 1 (list) or 2 (auto) (got %d)", o->exchange);
   return BFS_OK;
 }
 
@@ -361,6 +363,194 @@ static inline int ev_rec(Graph& G, int level, int p) {
   return BFS_OK;
 }
 
+// ------------------------------------------------------------------ list exchange (NEXT-1)
+// The paper's per-phase choice between a list of indices and a bitmap: a message of
+// n indices over an index space of L = block vertices is a list iff n <= T = L/32 words (the
+// bitmap's size, strict ">" for the bitmap).  Message sizes depend on counts,
+// so both phases first exchange the counts and read them on the host (host-driven level loop).
+static int alloc_xchg(Graph& G) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  const uint64_t S = (uint64_t)(g.R > g.C ? g.R : g.C);
+  int rc;
+  for (Rank& rk : G.ranks) {
+    if (rk.xsend) continue;
+    // a list holds up to `block` indices (forced list mode on a dense level)
+    if ((rc = G_alloc(G, (void**)&rk.xsend, S * g.block * 4 + 16))) return rc;
+    if ((rc = G_alloc(G, (void**)&rk.xrecv, S * g.block * 4 + 16))) return rc;
+    if ((rc = G_alloc(G, (void**)&rk.xoff, S * W * 4 + 16))) return rc;
+    if ((rc = G_alloc(G, (void**)&rk.xcnt, 64 * 8))) return rc;
+    rk.xtmp_bytes = list_encode_tmp_bytes(S * W);
+    if ((rc = G_alloc(G, &rk.xtmp, rk.xtmp_bytes ? rk.xtmp_bytes : 16))) return rc;
+  }
+  return BFS_OK;
+}
+
+static bool use_list(const Graph& G, uint64_t n) {
+  return G.opts.exchange == BFS_XCHG_LIST || (G.opts.exchange == BFS_XCHG_AUTO && n <= G.g.words_block());
+}
+
+// column phase: the R owned frontier segments of a grid column, gathered into all_front
+static int expand_exchange_x(Graph& G) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  cudaStream_t s = G.stream;
+  if (g.R == 1) return BFS_OK;
+  // counts of every rank of each local column, on the host: h[i] for column rank i
+  std::vector<ull> cnt((size_t)G.ranks.size() * 64, 0);
+  for (Rank& rk : G.ranks) {
+    CKR(cudaMemsetAsync(rk.xcnt, 0, 64 * 8, s));
+    CKR(launch_seg_popc(rk.all_front + (uint64_t)rk.i * W, W, 1, rk.xcnt, s));
+  }
+  if (G.world_size > 1) {
+    Rank& rk = G.ranks[0];
+    NKR(ncclAllGather(rk.xcnt, rk.xcnt + 1, 1, ncclUint64, G.colc, s));  // R <= 63 counts
+    CKR(cudaMemcpyAsync(cnt.data(), rk.xcnt + 1, g.R * 8, cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  } else {
+    for (size_t k = 0; k < G.ranks.size(); ++k)
+      CKR(cudaMemcpyAsync(&cnt[k * 64], G.ranks[k].xcnt, 8, cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  }
+  auto n_of = [&](const Rank& dst, int i2) -> ull {  // count of column rank i2 of dst's column
+    if (G.world_size > 1) return cnt[i2];
+    for (size_t k = 0; k < G.ranks.size(); ++k)
+      if (G.ranks[k].j == dst.j && G.ranks[k].i == i2) return cnt[k * 64];
+    return 0;
+  };
+  // one encoding per phase and column (an all-gather has one message size): the largest count
+  for (Rank& dst : G.ranks) {
+    ull maxn = 0;
+    for (int i2 = 0; i2 < g.R; ++i2) maxn = n_of(dst, i2) > maxn ? n_of(dst, i2) : maxn;
+    if (!use_list(G, maxn)) {
+      if (G.world_size > 1) {
+        NKR(ncclAllGather(dst.all_front + (uint64_t)dst.i * W, dst.all_front, W, ncclUint32, G.colc, s));
+      } else {
+        for (int i2 = 0; i2 < g.R; ++i2) {
+          if (i2 == dst.i) continue;
+          const Rank& src = G.ranks[dst.j * g.R + i2];
+          CKR(cudaMemcpyAsync(dst.all_front + i2 * W, src.all_front + i2 * W, W * 4, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+      G.xbytes += (ull)(g.R - 1) * W * 4;
+      continue;
+    }
+    G.xlists += (ull)(g.R - 1);
+    if (G.world_size > 1) {
+      CKR(launch_list_encode(dst.all_front + (uint64_t)dst.i * W, W, 1, dst.xoff, dst.xtmp, dst.xtmp_bytes, dst.xsend,
+                             g.block, s));
+      if (maxn) NKR(ncclAllGather(dst.xsend, dst.xrecv, maxn, ncclUint32, G.colc, s));
+    } else {
+      for (int i2 = 0; i2 < g.R; ++i2) {
+        if (i2 == dst.i) continue;
+        Rank& src = G.ranks[dst.j * g.R + i2];
+        CKR(launch_list_encode(src.all_front + (uint64_t)i2 * W, W, 1, src.xoff, src.xtmp, src.xtmp_bytes, src.xsend,
+                               g.block, s));
+        const ull n = n_of(dst, i2);
+        if (n) CKR(cudaMemcpyAsync(dst.xrecv + i2 * maxn, src.xsend, n * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    for (int i2 = 0; i2 < g.R; ++i2) {
+      if (i2 == dst.i) continue;
+      const ull n = n_of(dst, i2);
+      G.xbytes += n * 4;
+      CKR(cudaMemsetAsync(dst.all_front + i2 * W, 0, W * 4, s));
+      CKR(launch_list_scatter(dst.xrecv + i2 * maxn, n, dst.all_front + i2 * W, s));
+    }
+  }
+  return BFS_OK;
+}
+
+// row phase: P_ij sends its discovered rows of block (i,c) to P_ic, one message per pair, each
+// encoded by its own count
+static int fold_exchange_x(Graph& G) {
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  cudaStream_t s = G.stream;
+  if (g.C == 1) return BFS_OK;
+  const size_t nl = G.ranks.size();
+  // cnt[k*64 + c] = rows of segment c discovered by local rank k
+  std::vector<ull> cnt(nl * 64, 0), rcnt(64, 0);
+  for (Rank& rk : G.ranks) {
+    CKR(cudaMemsetAsync(rk.xcnt, 0, 64 * 8, s));
+    CKR(launch_seg_popc(rk.sendbuf, W, g.C, rk.xcnt, s));
+  }
+  if (G.world_size > 1) {
+    Rank& rk = G.ranks[0];
+    NKR(ncclGroupStart());  // counts: xcnt[c] = mine for c, xcnt[32 + c] = c's for me (C <= 32)
+    for (int c = 0; c < g.C; ++c) {
+      if (c == rk.j) continue;
+      NKR(ncclSend(rk.xcnt + c, 1, ncclUint64, c, G.rowc, s));
+      NKR(ncclRecv(rk.xcnt + 32 + c, 1, ncclUint64, c, G.rowc, s));
+    }
+    NKR(ncclGroupEnd());
+    std::vector<ull> h(64);
+    CKR(cudaMemcpyAsync(h.data(), rk.xcnt, 64 * 8, cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+    for (int c = 0; c < g.C; ++c) {
+      cnt[c] = h[c];
+      rcnt[c] = h[32 + c];
+    }
+  } else {
+    for (size_t k = 0; k < nl; ++k) CKR(cudaMemcpyAsync(&cnt[k * 64], G.ranks[k].xcnt, g.C * 8, cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  }
+  // encode every outgoing segment as a list (segments sent as bitmaps ignore theirs)
+  for (Rank& rk : G.ranks)
+    CKR(launch_list_encode(rk.sendbuf, W, g.C, rk.xoff, rk.xtmp, rk.xtmp_bytes, rk.xsend, g.block, s));
+  if (G.world_size > 1) {
+    Rank& rk = G.ranks[0];
+    NKR(ncclGroupStart());
+    for (int c = 0; c < g.C; ++c) {
+      if (c == rk.j) continue;
+      const ull n = cnt[c], nr = rcnt[c];
+      if (use_list(G, n)) {
+        if (n) NKR(ncclSend(rk.xsend + (uint64_t)c * g.block, n, ncclUint32, c, G.rowc, s));
+        G.xbytes += n * 4;
+        ++G.xlists;
+      } else {
+        NKR(ncclSend(rk.sendbuf + (uint64_t)c * W, W, ncclUint32, c, G.rowc, s));
+        G.xbytes += W * 4;
+      }
+      if (use_list(G, nr)) {
+        if (nr) NKR(ncclRecv(rk.xrecv + (uint64_t)c * g.block, nr, ncclUint32, c, G.rowc, s));
+      } else {
+        NKR(ncclRecv(rk.recv + (uint64_t)c * W, W, ncclUint32, c, G.rowc, s));
+      }
+    }
+    NKR(ncclGroupEnd());
+    for (int c = 0; c < g.C; ++c) {
+      if (c == rk.j || !use_list(G, rcnt[c])) continue;
+      CKR(cudaMemsetAsync(rk.recv + (uint64_t)c * W, 0, W * 4, s));
+      CKR(launch_list_scatter(rk.xrecv + (uint64_t)c * g.block, rcnt[c], rk.recv + (uint64_t)c * W, s));
+    }
+  } else {
+    for (size_t kd = 0; kd < nl; ++kd) {
+      Rank& dst = G.ranks[kd];
+      for (int c = 0; c < g.C; ++c) {
+        if (c == dst.j) continue;
+        const size_t ks = (size_t)c * g.R + dst.i;
+        const Rank& src = G.ranks[ks];
+        const ull n = cnt[ks * 64 + dst.j];
+        if (use_list(G, n)) {
+          G.xbytes += n * 4;
+          ++G.xlists;
+          if (n)
+            CKR(cudaMemcpyAsync(dst.xrecv + (uint64_t)c * g.block, src.xsend + (uint64_t)dst.j * g.block, n * 4,
+                                cudaMemcpyDeviceToDevice, s));
+          CKR(cudaMemsetAsync(dst.recv + (uint64_t)c * W, 0, W * 4, s));
+          CKR(launch_list_scatter(dst.xrecv + (uint64_t)c * g.block, n, dst.recv + (uint64_t)c * W, s));
+        } else {
+          G.xbytes += W * 4;
+          CKR(cudaMemcpyAsync(dst.recv + (uint64_t)c * W, src.sendbuf + (uint64_t)dst.j * W, W * 4,
+                              cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    }
+  }
+  return BFS_OK;
+}
+
 // ------------------------------------------------------------------ parent resolution (C > 1)
 static int resolve_parents(Graph& G) {
   const Geom& g = G.g;
@@ -440,7 +630,8 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const bool ev = !use_cond;
   int rc;
   if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
-  if ((rc = expand_exchange(G))) return rc;
+  const bool xl = G.opts.exchange != BFS_XCHG_BITMAP;  // never inside a graph capture
+  if ((rc = xl ? expand_exchange_x(G) : expand_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
   if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
@@ -448,7 +639,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
   if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
-  if ((rc = fold_exchange(G))) return rc;
+  if ((rc = xl ? fold_exchange_x(G) : fold_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 5))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_update(g, rk, G.d_ctrl, s));
   if (ev && (rc = ev_rec(G, nlev, 6))) return rc;
@@ -505,7 +696,10 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   int rc;
   // graph mode: no phase events, and not on the very first run (which initialises the kernels'
   // launch attributes outside of any capture)
-  bool use_graph = !G.opts.phase_timing && !G.graph_failed && G.runs > 0;
+  bool use_graph = !G.opts.phase_timing && !G.graph_failed && G.runs > 0 && G.opts.exchange == BFS_XCHG_BITMAP;
+  G.xbytes = G.xlists = 0;
+  const uint64_t xk0 = list_kernel_launches();
+  if (G.opts.exchange != BFS_XCHG_BITMAP && (rc = alloc_xchg(G))) return rc;
   if (use_graph && (!G.gexec || G.graph_stream != s || G.graph_E != G.opts.edges_per_thread)) {
     if (build_level_graph(G) != BFS_OK) {
       // orchestration fallback only (same kernels, host-driven loop); clear the sticky state
@@ -549,7 +743,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
-    par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : rk.parent_tmp;
+    par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : nullptr;  // no parent: not computed
     CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr, s));
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[2], s));
@@ -581,7 +775,8 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       stats->edges_scanned += G.lvl_edges[l];
       stats->frontier_columns += G.lvl_frontier[l];
     }
-    stats->bytes_exchanged = bytes;
+    stats->bytes_exchanged = G.opts.exchange == BFS_XCHG_BITMAP ? bytes : G.xbytes;
+    stats->list_messages = G.xlists;
     if (G.opts.phase_timing) {  // the stream is synchronised: reading the events costs nothing
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, G.tail_ev[0], G.tail_ev[1]);
@@ -595,7 +790,8 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     // req_build, 2 seg_totals and resp_pack.
     const uint64_t nl = G.ranks.size();
     stats->kernel_launches =
-        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0);
+        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0) +
+        (list_kernel_launches() - xk0);
   }
   return BFS_OK;
 }

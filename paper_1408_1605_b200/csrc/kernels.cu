@@ -1312,7 +1312,7 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
     const uint32_t p = pp[k];
     const bool reached = (a.vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
     int64_t v = -1;
-    if (reached) {
+    if (reached && parent_out) {  // without a parent output the resolution did not run
       const int c = a.winner ? (int)a.winner[p] : a.j;
       if (c == a.j) {
         v = (int64_t)a.pred_own[p];
@@ -1456,6 +1456,82 @@ __global__ void k_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned lo
   const int c = threadIdx.x;
   if (c < C) totals[c] = off[(uint64_t)(c + 1) * W] - off[(uint64_t)c * W];
 }
+// ------------------------------------------------------------------ list exchange
+// count of set bits of each of nseg segments of W words (grid.y = segment)
+__global__ void k_seg_popc(const uint32_t* __restrict__ bm, uint64_t W, ull* cnt) {
+  const uint64_t base = (uint64_t)blockIdx.y * W;
+  unsigned c = 0;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x)
+    c += __popc(bm[base + w]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + blockIdx.y, (ull)c);
+}
+
+static uint64_t g_list_launches = 0;  // kernels launched by the list-exchange launchers
+uint64_t list_kernel_launches() { return g_list_launches; }
+
+cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, ull* cnt, cudaStream_t s) {
+  if (!W || nseg <= 0) return cudaSuccess;
+  ++g_list_launches;
+  const uint64_t blocks = (W + 255) / 256;
+  k_seg_popc<<<dim3((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)nseg), 256, 0, s>>>(bm, W, cnt);
+  return cudaGetLastError();
+}
+
+// list of segment k (ascending local indices) at list[k*lstride + ...]; off = exclusive popcount
+// scan over all nseg*W words
+__global__ void k_list_write(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ off, uint64_t W,
+                             uint64_t nwords, uint64_t lstride, uint32_t* list) {
+  for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < nwords;
+       gid += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t b = bm[gid];
+    if (!b) continue;
+    const uint64_t k = gid / W, w = gid - k * W;
+    uint64_t pos = k * lstride + (off[gid] - off[k * W]);
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      list[pos++] = (uint32_t)(w * 32 + bit);
+    }
+  }
+}
+
+size_t list_encode_tmp_bytes(uint64_t nwords) {
+  size_t bytes = 0;
+  cub::TransformInputIterator<uint32_t, PopcOp, const uint32_t*> it(nullptr, PopcOp());
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (uint32_t*)nullptr, nwords, (cudaStream_t)0);
+  return bytes;
+}
+
+cudaError_t launch_list_encode(const uint32_t* bm, uint64_t W, int nseg, uint32_t* off, void* tmp, size_t tmp_bytes,
+                               uint32_t* list, uint64_t lstride, cudaStream_t s) {
+  const uint64_t nwords = W * (uint64_t)nseg;
+  if (!nwords) return cudaSuccess;
+  cub::TransformInputIterator<uint32_t, PopcOp, const uint32_t*> it(bm, PopcOp());
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, it, off, nwords, s);
+  if (e != cudaSuccess) return e;
+  ++g_list_launches;
+  k_list_write<<<num_sms() * 8, 256, 0, s>>>(bm, off, W, nwords, lstride, list);
+  return cudaGetLastError();
+}
+
+__global__ void k_list_scatter(const uint32_t* __restrict__ list, uint64_t n, uint32_t* bm) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = list[t];
+    atomicOr(bm + (x >> 5), 1u << (x & 31));
+  }
+}
+
+cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  ++g_list_launches;
+  const uint64_t blocks = (n + 255) / 256;
+  k_list_scatter<<<(unsigned)(blocks < (uint64_t)num_sms() * 8 ? blocks : (uint64_t)num_sms() * 8), 256, 0, s>>>(
+      list, n, bm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s) {
   k_seg_totals<<<1, 64, 0, s>>>(off, W, C, totals);
   return cudaGetLastError();

@@ -39,6 +39,16 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s);
 
 cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s);
 
+// List exchange (opts.exchange): per-segment set-bit counts (added into cnt[k]),
+// bitmap segments -> ascending local index lists (list segment k at k*lstride), and lists -> bits
+// (OR into a zeroed bitmap segment).
+cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, unsigned long long* cnt, cudaStream_t s);
+size_t list_encode_tmp_bytes(uint64_t nwords);
+cudaError_t launch_list_encode(const uint32_t* bm, uint64_t W, int nseg, uint32_t* off, void* tmp, size_t tmp_bytes,
+                               uint32_t* list, uint64_t lstride, cudaStream_t s);
+cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, cudaStream_t s);
+uint64_t list_kernel_launches();  // running count of the three launchers' kernels (process-wide)
+
 // m_comp: sum of tdeg over reached owned vertices into *out (device u64).
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, unsigned long long* out, cudaStream_t s);
 

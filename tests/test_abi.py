@@ -42,8 +42,9 @@ def test_struct_layout_matches_header(L):
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(bfs_comm), sizeof(bfs_opts), sizeof(bfs_info), sizeof(bfs_stats),
          sizeof(bfs_level_record));
-  printf("%zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
-         offsetof(bfs_level_record, edges));
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
+         offsetof(bfs_level_record, edges), offsetof(bfs_opts, exchange), offsetof(bfs_stats, list_messages),
+         offsetof(bfs_stats, kernel_launches));
   return 0;
 }
 '''
@@ -56,7 +57,8 @@ int main(void) {
     sizes = [int(x) for x in out]
     assert sizes[:5] == [ctypes.sizeof(bfs.Comm), ctypes.sizeof(bfs.Opts), ctypes.sizeof(bfs.Info),
                          ctypes.sizeof(bfs.Stats), ctypes.sizeof(bfs.LevelRecord)]
-    assert sizes[5:] == [bfs.Info.nout.offset, bfs.Stats.bytes_exchanged.offset, bfs.LevelRecord.edges.offset]
+    assert sizes[5:] == [bfs.Info.nout.offset, bfs.Stats.bytes_exchanged.offset, bfs.LevelRecord.edges.offset,
+                         bfs.Opts.exchange.offset, bfs.Stats.list_messages.offset, bfs.Stats.kernel_launches.offset]
 
 
 def test_strerror_and_null_args(L):

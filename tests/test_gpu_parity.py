@@ -154,6 +154,68 @@ def test_degree_matches_oracle(bfs):
             assert g.degree(v) == deg[v]
 
 
+# ---------------------------------------------------------------- list <-> bitmap exchange (NEXT-1)
+@pytest.mark.parametrize("exchange", ["list", "auto"])
+@pytest.mark.parametrize("grid", [(1, 2), (2, 1), (2, 2), (2, 4), (4, 2)])
+def test_exchange_modes(bfs, exchange, grid):
+    """Index-list and auto (P:874-897 threshold T = block/32) messages give the same outputs;
+    byte counts follow the encoding."""
+    scale = 12
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    og = oracle.Graph(n, s, d)
+    g = make_graph(bfs, s, d, n, *grid)
+    roots = inputs.sample_roots(n, 6, inputs.nonisolated_mask(n, s, d))
+    g.set_opts(bfs.make_opts(edges_per_thread=4))
+    bitmap_bytes = g.run(roots[0]).bytes_exchanged
+    g.set_opts(bfs.make_opts(edges_per_thread=4, exchange=exchange))
+    for r in roots:
+        check_root(g, og, r, n)
+    st = g.run(roots[0])
+    R, C = grid
+    nmsg = st.nlevels * R * C * ((R - 1) + (C - 1))  # per-level messages of all ranks
+    if exchange == "list":
+        assert st.list_messages == nmsg
+        # every list entry is one discovered/frontier vertex: at most 4 B per reached vertex per
+        # receiving peer and level
+        assert 0 < st.bytes_exchanged <= 4 * n * max(R, C) * st.nlevels
+    else:
+        assert 0 < st.list_messages < nmsg  # sparse levels as lists, the dense ones as bitmaps
+        assert st.bytes_exchanged < bitmap_bytes
+
+
+def test_exchange_threshold_rule(bfs):
+    """a message is a list iff n <= T = L/32 words (L = block), strictly '>' for
+    the bitmap.  A 2x1 grid (one column phase message per rank and level) on a star whose hub's
+    frontier sizes are known exactly."""
+    R, C = 2, 1
+    nverts = 4096  # block = 2048 vertices, T = 64 words
+    hub = 0
+    # level 1 frontier on the owner of block 1: exactly 64 leaves there (list), then 65 (bitmap)
+    for k, expect_list in ((64, True), (65, False)):
+        leaves = np.arange(2048, 2048 + k, dtype=np.uint64)
+        t = np.stack([np.full(k, hub, dtype=np.uint64), leaves], 1)
+        og = oracle.Graph(nverts, t[:, 0], t[:, 1])
+        g = make_graph(bfs, t[:, 0], t[:, 1], nverts, R, C)
+        g.set_opts(bfs.make_opts(edges_per_thread=4, exchange="auto"))
+        check_root(g, og, hub, nverts)
+        st = g.run(hub)
+        # one all-gather per level, 2 messages, both encoded by the larger count: frontier sizes
+        # per level are 1 (the hub), k (the leaves), then 0
+        f = [1, k] + [0] * st.nlevels
+        assert st.list_messages == sum(2 for lv in range(st.nlevels) if f[lv] <= 64)
+        assert (f[1] <= 64) == expect_list
+
+
+def test_exchange_invalid(bfs):
+    s = np.array([0], dtype=np.uint64)
+    d = np.array([1], dtype=np.uint64)
+    g = make_graph(bfs, s, d, 8)
+    with pytest.raises(bfs.BfsError) as e:
+        g.set_opts(bfs.make_opts(exchange=3))
+    assert e.value.status == bfs.BFS_EINVAL
+
+
 # ---------------------------------------------------------------- edge cases
 def test_padding_and_tiny_graphs(bfs):
     # nverts not a multiple of 32*R*C; single vertex; no edges
