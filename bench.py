@@ -176,6 +176,7 @@ def workload_config(args, world):
     scale = args.scale if args.scale else 26 + int(round(math.log2(world)))
     return {"workload": f"graph500-kronecker-s{scale}-ef16-{R}x{C}", "scale": scale, "edgefactor": 16,
             "grid": f"{R}x{C}", "roots": 64, "parallelism": f"2d-{R}x{C}", "edges_per_thread": args.E,
+            "exchange": getattr(args, "exchange", "bitmap"),
             "l2": "flushed between steps (256 MiB write); graph > L2"}
 
 
@@ -199,8 +200,10 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     # timed steps: the level loop runs as one CUDA graph (no phase events); the per-phase CUDA-event
     # times (roofline of the expansion kernel) come from a replay of the same roots afterwards
-    opts = bfs.make_opts(edges_per_thread=args.E, phase_timing=False, stream=stream.cuda_stream)
-    opts_phase = bfs.make_opts(edges_per_thread=args.E, phase_timing=True, stream=stream.cuda_stream)
+    opts = bfs.make_opts(edges_per_thread=args.E, phase_timing=False, stream=stream.cuda_stream,
+                         exchange=args.exchange)
+    opts_phase = bfs.make_opts(edges_per_thread=args.E, phase_timing=True, stream=stream.cuda_stream,
+                               exchange=args.exchange)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -237,7 +240,7 @@ def run_ours(args, rank, world, local_rank):
         g.run(warm_roots[k % len(warm_roots)], parent, level)
     torch.cuda.synchronize()
 
-    times, mcomps, launches = [], [], 0
+    times, mcomps, launches, xbytes, xlists = [], [], 0, 0, 0
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             r = timed_roots[k % len(timed_roots)]
@@ -252,6 +255,8 @@ def run_ours(args, rank, world, local_rank):
             t_ms = max_over_ranks(ev0.elapsed_time(ev1))
             times.append(t_ms)
             launches += st.kernel_launches
+            xbytes += st.bytes_exchanged
+            xlists += st.list_messages
             mcomps.append(g.mcomp())
     clocks = clk.summary()
     teps = [m / (t * 1e-3) for m, t in zip(mcomps, times)]
@@ -326,6 +331,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8,
                 "d2h_bytes_per_step": int(info.nout) * 8 * world, "result": "parent array (int64 per vertex)"},
         "gpu_launches": int(launches),
+        "exchange": {"mode": args.exchange, "bytes_per_step_rank0": xbytes / max(1, args.steps),
+                     "list_messages_per_step_rank0": xlists / max(1, args.steps)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "k_expand (frontier expansion, Alg.3)", "peak_kind": peak_kind,
@@ -358,6 +365,8 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--E", type=int, default=4)
     ap.add_argument("--grid", default="", help="RxC override of the default grid (1x1, 1x2, 2x2, 2x4)")
+    ap.add_argument("--exchange", default="bitmap", choices=["bitmap", "list", "auto"],
+                    help="per-level message encoding (bitmap: CUDA-graph level loop; list/auto: host-sized)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase-timing", action="store_true", help="(diagnostic) no per-phase events")
     args = ap.parse_args()
