@@ -13,7 +13,7 @@
 namespace bfs200 {
 
 constexpr uint32_t kNoPred = 0xFFFFFFFFu;  // "no candidate" sentinel in pred[] (R11)
-constexpr int kScanSegWords = 256;         // bitmap words per warp segment of the unpack/scan (8192 vertices)
+constexpr int kScanSegWords = 128;         // bitmap words per warp segment of the unpack/scan (4096 vertices)
 constexpr int kScanThreads = 256;          // 8 warps = 8 segments per CTA
 constexpr int kExpandThreads = 256;
 constexpr int kMaxLevels = 4096;
