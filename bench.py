@@ -177,6 +177,8 @@ def workload_config(args, world):
     return {"workload": f"graph500-kronecker-s{scale}-ef16-{R}x{C}", "scale": scale, "edgefactor": 16,
             "grid": f"{R}x{C}", "roots": 64, "parallelism": f"2d-{R}x{C}", "edges_per_thread": args.E,
             "exchange": getattr(args, "exchange", "bitmap"),
+            "transport": ("nvlink-peer" if getattr(args, "transport", "peer") == "peer" and
+                          getattr(args, "exchange", "bitmap") == "bitmap" else "nccl") if world > 1 else "none",
             "l2": "flushed between steps (256 MiB write); graph > L2"}
 
 
@@ -201,9 +203,9 @@ def run_ours(args, rank, world, local_rank):
     # timed steps: the level loop runs as one CUDA graph (no phase events); the per-phase CUDA-event
     # times (roofline of the expansion kernel) come from a replay of the same roots afterwards
     opts = bfs.make_opts(edges_per_thread=args.E, phase_timing=False, stream=stream.cuda_stream,
-                         exchange=args.exchange)
+                         exchange=args.exchange, peer_exchange=args.transport == "peer" and args.exchange == "bitmap")
     opts_phase = bfs.make_opts(edges_per_thread=args.E, phase_timing=True, stream=stream.cuda_stream,
-                               exchange=args.exchange)
+                               exchange=args.exchange, peer_exchange=args.transport == "peer" and args.exchange == "bitmap")
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -367,6 +369,9 @@ def main():
     ap.add_argument("--grid", default="", help="RxC override of the default grid (1x1, 1x2, 2x2, 2x4)")
     ap.add_argument("--exchange", default="bitmap", choices=["bitmap", "list", "auto"],
                     help="per-level message encoding (bitmap: CUDA-graph level loop; list/auto: host-sized)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: per-level exchanges over NVLink peer memory (opts.peer_exchange, default) "
+                         "or NCCL collectives")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase-timing", action="store_true", help="(diagnostic) no per-phase events")
     args = ap.parse_args()

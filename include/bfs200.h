@@ -77,6 +77,15 @@ typedef struct {
                            1 and 2 size the messages on the host each level (host-driven loop, one
                            count exchange + device-to-host read per phase). Values are otherwise
                            BFS_EINVAL. Results are identical in every mode. */
+  int peer_exchange;    /* 1: per-level exchanges over NVLink peer memory instead of NCCL
+                           collectives (§8(f) NEXT-2): the parent pass (K4) stores the fold
+                           message straight into the owners' receive buffers, the update (K2)
+                           stores the next frontier segment into the column peers' frontier
+                           bitmaps, and two cross-GPU flag barriers per level (the second also
+                           sums the new-vertex counts) replace the all-gather, the send/recv and
+                           the all-reduce.  Needs CUDA IPC / peer access between the ranks' GPUs
+                           (set up collectively on the first run) and exchange = 0; ignored by
+                           loopback and 1x1.  0 (default): NCCL collectives. */
 } bfs_opts;
 
 enum { BFS_XCHG_BITMAP = 0, BFS_XCHG_LIST = 1, BFS_XCHG_AUTO = 2 };

@@ -33,7 +33,7 @@ class Comm(ctypes.Structure):
 
 class Opts(ctypes.Structure):
     _fields_ = [("edges_per_thread", ctypes.c_int), ("phase_timing", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("exchange", ctypes.c_int)]
+                ("exchange", ctypes.c_int), ("peer_exchange", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -133,8 +133,9 @@ XCHG_BITMAP, XCHG_LIST, XCHG_AUTO = 0, 1, 2
 XCHG = {"bitmap": XCHG_BITMAP, "list": XCHG_LIST, "auto": XCHG_AUTO}
 
 
-def make_opts(edges_per_thread=4, phase_timing=False, stream=None, exchange="bitmap") -> Opts:
+def make_opts(edges_per_thread=4, phase_timing=False, stream=None, exchange="bitmap", peer_exchange=False) -> Opts:
     o = Opts()
+    o.peer_exchange = 1 if peer_exchange else 0
     o.edges_per_thread = int(edges_per_thread)
     o.phase_timing = 1 if phase_timing else 0
     o.exchange = XCHG[exchange] if isinstance(exchange, str) else int(exchange)

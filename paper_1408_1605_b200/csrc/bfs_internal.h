@@ -37,6 +37,12 @@ struct LevelInfo {
   unsigned long long pad[6];
 };
 
+// One slot of the peer-exchange signal array (one slot per sending rank).
+struct XSig {
+  unsigned long long flag;  // epoch of the sender's last barrier
+  unsigned long long val;   // the sender's value for that barrier (new-vertex count)
+};
+
 // Device-side level loop state (the loop may run as a CUDA-graph WHILE node).
 struct LevelCtrl {
   uint32_t lvl;   // level being assigned (1 for the root's neighbours)
@@ -115,6 +121,9 @@ struct Rank {
   void* xtmp = nullptr;          // CUB temporary storage of that scan
   size_t xtmp_bytes = 0;
   unsigned long long* xcnt = nullptr;  // [64] per-segment counts (device)
+  // peer exchange (opts.peer_exchange): device arrays of peer pointers, null when inactive
+  uint32_t** fold_dst = nullptr;  // [C] recv of P_ic + j*W (null for c == j)
+  uint32_t** exp_dst = nullptr;   // [R] all_front of P_(i2)j + i*W (null for i2 == i)
   unsigned long long* scratch = nullptr;  // small reduction scratch
 };
 
@@ -152,11 +161,19 @@ struct Graph {
   cudaGraphConditionalHandle cond = 0;
   cudaStream_t graph_stream = nullptr;
   int graph_E = 0;
+  bool graph_peer = false;  // the captured level used the peer exchange
   bool graph_failed = false;
   int runs = 0;
   int ev_levels = 0;
   std::vector<uint64_t> lvl_frontier, lvl_edges;
   uint64_t xbytes = 0, xlists = 0;  // list exchange: bytes sent and list messages in this run
+  // peer exchange (NEXT-2): NVLink peer mappings of every rank's signal array, set up on first use
+  bool peer_ready = false;
+  XSig* xsig = nullptr;               // [64] this rank's signal array (slot = sender world rank)
+  XSig** d_sig_peers = nullptr;       // [world] device array: every rank's signal array (mapped)
+  unsigned long long* d_epoch = nullptr;
+  int* d_xerr = nullptr;
+  std::vector<void*> ipc_opened;      // cudaIpcOpenMemHandle mappings to close
 };
 
 }  // namespace bfs200

@@ -226,6 +226,8 @@ static void release_graph(Graph* G) {
   if (!G) return;
   cudaSetDevice(G->device);
   if (G->stream) cudaStreamSynchronize(G->stream);
+  for (void* p : G->ipc_opened) cudaIpcCloseMemHandle(p);
+  G->ipc_opened.clear();
   for (void* p : G->allocs) cudaFree(p);
   G->allocs.clear();
   for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
@@ -254,6 +256,10 @@ static int check_opts(const bfs_opts* o) {
     return set_err(BFS_EINVAL, "edges_per_thread must be 1, 2, 4, 8 or 16 (got %d)", E);
   if (o->exchange < BFS_XCHG_BITMAP || o->exchange > BFS_XCHG_AUTO)
     return set_err(BFS_EINVAL, "exchange must be 0 (bitmap), 1 (list) or 2 (auto) (got %d)", o->exchange);
+  if (o->peer_exchange != 0 && o->peer_exchange != 1)
+    return set_err(BFS_EINVAL, "peer_exchange must be 0 or 1 (got %d)", o->peer_exchange);
+  if (o->peer_exchange && o->exchange != BFS_XCHG_BITMAP)
+    return set_err(BFS_EINVAL, "peer_exchange needs exchange = 0 (bitmap messages)");
   return BFS_OK;
 }
 
@@ -360,6 +366,85 @@ static inline int ev_rec(Graph& G, int level, int p) {
   int rc = ev_prepare(G, level);
   if (rc) return rc;
   CKR(cudaEventRecord(G.ev[(size_t)level * kPhaseEvents + p], G.stream));
+  return BFS_OK;
+}
+
+// ------------------------------------------------------------------ peer exchange (NEXT-2)
+// CUDA IPC handles of every rank's recv, all_front and signal array are all-gathered over the
+// world communicator and opened; each rank then holds device tables of the peer pointers its
+// kernels store into (fold: recv of P_ic; expand: all_front of P_(i2)j) and of the signal arrays.
+static bool peer_active(const Graph& G) {
+  return G.opts.peer_exchange && G.world_size > 1 && G.opts.exchange == BFS_XCHG_BITMAP;
+}
+
+static int setup_peer(Graph& G) {
+  if (G.peer_ready) return BFS_OK;
+  const Geom& g = G.g;
+  const uint64_t W = g.words_block();
+  const int P = G.world_size, me = G.world_rank;
+  cudaStream_t s = G.stream;
+  Rank& rk = G.ranks[0];
+  int rc;
+  if ((rc = G_alloc(G, (void**)&G.xsig, 64 * sizeof(XSig)))) return rc;
+  CKR(cudaMemset(G.xsig, 0, 64 * sizeof(XSig)));
+  if ((rc = G_alloc(G, (void**)&G.d_epoch, 8))) return rc;
+  CKR(cudaMemset(G.d_epoch, 0, 8));
+  if ((rc = G_alloc(G, (void**)&G.d_xerr, 8))) return rc;
+  CKR(cudaMemset(G.d_xerr, 0, 8));
+  if (!rk.recv) {  // C == 1: no fold buffer; a dummy keeps the handle layout uniform
+    if ((rc = G_alloc(G, (void**)&rk.recv, 16))) return rc;
+  }
+  cudaIpcMemHandle_t mine[3];
+  CKR(cudaIpcGetMemHandle(&mine[0], rk.recv));
+  CKR(cudaIpcGetMemHandle(&mine[1], rk.all_front));
+  CKR(cudaIpcGetMemHandle(&mine[2], G.xsig));
+  const size_t hb = sizeof(mine);
+  unsigned char* dbuf = nullptr;
+  CKR(cudaMalloc(&dbuf, hb * (P + 1)));
+  CKR(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice));
+  NKR(ncclAllGather(dbuf, dbuf + hb, hb, ncclUint8, G.world, s));
+  std::vector<cudaIpcMemHandle_t> all((size_t)P * 3);
+  CKR(cudaMemcpyAsync(all.data(), dbuf + hb, hb * P, cudaMemcpyDeviceToHost, s));
+  CKR(cudaStreamSynchronize(s));
+  cudaFree(dbuf);
+  std::vector<void*> recv_of(P), front_of(P), sig_of(P);
+  for (int p = 0; p < P; ++p) {
+    if (p == me) {
+      recv_of[p] = rk.recv;
+      front_of[p] = rk.all_front;
+      sig_of[p] = G.xsig;
+      continue;
+    }
+    for (int k = 0; k < 3; ++k) {
+      void* ptr = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)p * 3 + k], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(BFS_ECUDA, "peer_exchange: cudaIpcOpenMemHandle of rank %d failed: %s", p,
+                       cudaGetErrorString(e));
+      }
+      G.ipc_opened.push_back(ptr);
+      (k == 0 ? recv_of : k == 1 ? front_of : sig_of)[p] = ptr;
+    }
+  }
+  // tables: fold_dst[c] = recv of P_ic + j*W; exp_dst[i2] = all_front of P_(i2)j + i*W
+  std::vector<uint32_t*> fold((size_t)g.C, nullptr), expd((size_t)g.R, nullptr);
+  for (int c = 0; c < g.C; ++c)
+    if (c != rk.j) fold[c] = static_cast<uint32_t*>(recv_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
+  for (int i2 = 0; i2 < g.R; ++i2)
+    if (i2 != rk.i) expd[i2] = static_cast<uint32_t*>(front_of[rk.j * g.R + i2]) + (uint64_t)rk.i * W;
+  std::vector<XSig*> sigs(P);
+  for (int p = 0; p < P; ++p) sigs[p] = static_cast<XSig*>(sig_of[p]);
+  if ((rc = G_alloc(G, (void**)&rk.fold_dst, g.C * sizeof(uint32_t*)))) return rc;
+  if ((rc = G_alloc(G, (void**)&rk.exp_dst, g.R * sizeof(uint32_t*)))) return rc;
+  if ((rc = G_alloc(G, (void**)&G.d_sig_peers, P * sizeof(XSig*)))) return rc;
+  CKR(cudaMemcpy(rk.fold_dst, fold.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  CKR(cudaMemcpy(rk.exp_dst, expd.data(), g.R * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  CKR(cudaMemcpy(G.d_sig_peers, sigs.data(), P * sizeof(XSig*), cudaMemcpyHostToDevice));
+  // the peers' arrays must be zero (epochs start at 0) before anyone signals
+  NKR(ncclAllReduce(G.d_xerr, G.d_xerr, 1, ncclInt, ncclSum, G.world, s));
+  CKR(cudaStreamSynchronize(s));
+  G.peer_ready = true;
   return BFS_OK;
 }
 
@@ -629,6 +714,29 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const uint32_t tile_edges = expand_tile_edges(E);
   const bool ev = !use_cond;
   int rc;
+  if (peer_active(G)) {
+    // NEXT-2: the column all-gather happened in the previous level's K2 (peer stores), the fold
+    // in K4; two flag barriers replace the collectives (the second sums the new-vertex counts)
+    Rank& rk = G.ranks[0];
+    if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
+    if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
+    CKR(launch_scan(g, rk, tile_edges, s));
+    if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
+    CKR(launch_expand(g, rk, E, G.hot_h, s));
+    if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
+    CKR(launch_parent(g, rk, s));
+    if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
+    // barrier 1: every fold store has landed, and every rank is done reading its frontier bitmap
+    // (K2's peer stores below overwrite it)
+    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, false, G.d_xerr, s));
+    if (ev && (rc = ev_rec(G, nlev, 5))) return rc;
+    CKR(launch_update(g, rk, G.d_ctrl, s));
+    if (ev && (rc = ev_rec(G, nlev, 6))) return rc;
+    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, true, G.d_xerr, s));
+    CKR(launch_level_end(G.d_ctrl, G.infos, 1, true, G.cond, use_cond, s));
+    if (ev && (rc = ev_rec(G, nlev, 7))) return rc;
+    return BFS_OK;
+  }
   if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
   const bool xl = G.opts.exchange != BFS_XCHG_BITMAP;  // never inside a graph capture
   if ((rc = xl ? expand_exchange_x(G) : expand_exchange(G))) return rc;
@@ -679,6 +787,7 @@ static int build_level_graph(Graph& G) {
   CKR(cudaGraphInstantiate(&G.gexec, G.graph, 0));
   G.graph_stream = G.stream;
   G.graph_E = G.opts.edges_per_thread;
+  G.graph_peer = peer_active(G);
   return BFS_OK;
 }
 
@@ -688,9 +797,15 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   const uint64_t W = g.words_block();
   const uint64_t owner = root / g.block;
   bool owner_local = false;
+  int rcp;
+  if (peer_active(G) && (rcp = setup_peer(G))) return rcp;
   for (Rank& rk : G.ranks) {
     owner_local |= (uint64_t)rk.r == owner;
     CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, s));
+    // peer exchange: no all-gather before level 1, so the owner's column peers seed the bit
+    const int owner_i = (int)(owner % (uint64_t)g.R), owner_j = (int)(owner / (uint64_t)g.R);
+    if (peer_active(G) && (uint64_t)rk.r != owner && rk.j == owner_j)
+      CKR(launch_seed_col(rk.all_front, G.perm_fwd, root, g.block, owner_i, s));
   }
   CKR(launch_level_begin(G.d_ctrl, s));
   int rc;
@@ -700,7 +815,8 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   G.xbytes = G.xlists = 0;
   const uint64_t xk0 = list_kernel_launches();
   if (G.opts.exchange != BFS_XCHG_BITMAP && (rc = alloc_xchg(G))) return rc;
-  if (use_graph && (!G.gexec || G.graph_stream != s || G.graph_E != G.opts.edges_per_thread)) {
+  if (use_graph && (!G.gexec || G.graph_stream != s || G.graph_E != G.opts.edges_per_thread ||
+                    G.graph_peer != peer_active(G))) {
     if (build_level_graph(G) != BFS_OK) {
       // orchestration fallback only (same kernels, host-driven loop); clear the sticky state
       G.graph_failed = true;
@@ -720,6 +836,15 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
       CKR(cudaStreamSynchronize(s));
       if (G.h_ctrl->done) break;
+    }
+  }
+  if (peer_active(G)) {  // a barrier that timed out leaves the level loop undefined
+    int xerr = 0;
+    CKR(cudaMemcpyAsync(&xerr, G.d_xerr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+    if (xerr) {
+      G.broken = true;
+      return set_err(BFS_ENCCL, "peer_exchange: a cross-GPU barrier timed out (a peer stopped)");
     }
   }
   // outputs
@@ -789,9 +914,12 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     // scan(4) + expand + parent + update, then finalize; with C > 1 the resolution adds
     // req_build, 2 seg_totals and resp_pack.
     const uint64_t nl = G.ranks.size();
+    const bool peer = peer_active(G);
+    const int owner_j = (int)(owner / (uint64_t)g.R);
     stats->kernel_launches =
         (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0) +
-        (list_kernel_launches() - xk0);
+        (list_kernel_launches() - xk0) +
+        (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
   }
   return BFS_OK;
 }

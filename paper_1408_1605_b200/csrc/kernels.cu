@@ -994,7 +994,8 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
                                                                uint32_t* pmin, uint32_t* sendbuf,
                                                                const uint32_t* __restrict__ inv_col,
                                                                LevelInfo* info, uint32_t hot_words, int R,
-                                                               uint64_t Wc, int blog) {
+                                                               uint64_t Wc, int blog,
+                                                               uint32_t* const* __restrict__ fold_dst) {
   extern __shared__ __align__(16) unsigned char psmem[];
   uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
@@ -1040,12 +1041,20 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
       if (w < nwords) {
         vd[2 * w + 1] = myd;
         if (sendbuf) sendbuf[w] = myd;
+        if (fold_dst) {  // peer exchange: the fold message goes straight into the owner's recv
+          const uint64_t c = w / Wc;
+          if (fold_dst[c]) fold_dst[c][w - c * Wc] = myd;
+        }
       }
       ndisc += __popc(myd);
       continue;
     }
     const uint32_t d = (w < nwords) ? vd[2 * w + 1] : 0u;
     if (sendbuf && w < nwords) sendbuf[w] = d;
+    if (fold_dst && w < nwords) {  // peer exchange (NVLink stores): segment c -> recv of P_ic
+      const uint64_t c = w / Wc;
+      if (fold_dst[c]) fold_dst[c][w - c * Wc] = d;
+    }
     ndisc += __popc(d);
     if (!__any_sync(0xFFFFFFFFu, d != 0)) continue;
     if (p1) {
@@ -1132,6 +1141,10 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
 #pragma unroll
   for (int o = 16; o; o >>= 1) ndisc += __shfl_xor_sync(0xFFFFFFFFu, ndisc, o);
   if (lane == 0 && ndisc) atomicAdd(&info->disc_total, (ull)ndisc);
+  if (fold_dst) {  // the CTA's peer stores, then one system-scope fence (cumulative) before the flag
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
 }
 
 cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
@@ -1156,7 +1169,8 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   }
   k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
                                                         rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
-                                                        (uint32_t)hw, g.R, g.words_block(), blog);
+                                                        (uint32_t)hw, g.R, g.words_block(), blog,
+                                                        g.C > 1 ? rk.fold_dst : nullptr);
   return cudaGetLastError();
 }
 
@@ -1167,7 +1181,8 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
 // rows this rank discovered as visited so they are sent at most once.
 __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* recv, uint32_t* front_seg,
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
-                                                int j, const LevelCtrl* ctrl) {
+                                                int j, const LevelCtrl* ctrl, uint32_t* const* __restrict__ exp_dst,
+                                                int R) {
   // grid: x over the words of one segment, y = segment m (no 64-bit division)
   const int lvl = (int)ctrl->lvl;  // the level being assigned (device-side: the loop may be a graph)
   const int m = (int)blockIdx.y;
@@ -1196,6 +1211,9 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
     newbits = claimed;
     if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
     front_seg[w] = newbits;
+    if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
+      for (int i2 = 0; i2 < R; ++i2)
+        if (exp_dst[i2]) exp_dst[i2][w] = newbits;
   } else if (w < W) {
     const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
     if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
@@ -1224,13 +1242,18 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&info->newv, (ull)cnt);
+  if (exp_dst) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
 }
 
 cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s) {
   const uint64_t W = g.words_block();
   const dim3 grid((unsigned)((W + 255) / 256), (unsigned)g.C);
   k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
-                                g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, ctrl);
+                                g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, ctrl,
+                                g.R > 1 ? rk.exp_dst : nullptr, g.R);
   return cudaGetLastError();
 }
 
@@ -1456,6 +1479,70 @@ __global__ void k_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned lo
   const int c = threadIdx.x;
   if (c < C) totals[c] = off[(uint64_t)(c + 1) * W] - off[(uint64_t)c * W];
 }
+// ------------------------------------------------------------------ peer exchange (NEXT-2)
+// Cross-GPU barrier over NVLink peer memory: every rank stores (value, epoch) into its slot of
+// every peer's signal array (release, system scope), then waits until every peer's slot of its
+// own array carries the epoch (acquire).  Epochs come from a device counter that every rank
+// advances identically, so the barrier also works inside the CUDA-graph level loop.  With
+// sum_newv the values are the ranks' new-vertex counts and the sum replaces info->newv (the
+// termination reduction).  A bounded spin sets *err instead of hanging.
+__global__ void k_xbarrier(XSig* local, XSig* const* peers, int nranks, int me, ull* epoch_ctr, LevelInfo* info,
+                           int sum_newv, int* err) {
+  if (threadIdx.x != 0) return;
+  const ull epoch = ++(*epoch_ctr);
+  if (*(volatile int*)err) {  // an earlier barrier timed out: end the level loop (newv = 0)
+    if (sum_newv) info->newv = 0;
+    return;
+  }
+  const ull mine = sum_newv ? info->newv : 0ull;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int p = 0; p < nranks; ++p) {
+    if (p == me) continue;
+    XSig* dst = peers[p] + me;
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&dst->val), "l"(mine) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&dst->flag), "l"(epoch) : "memory");
+  }
+  ull total = mine;
+  const long long t0 = clock64();
+  for (int p = 0; p < nranks; ++p) {
+    if (p == me) continue;
+    ull f = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(&local[p].flag) : "memory");
+      if (f >= epoch) break;
+      if (clock64() - t0 > (1ll << 35)) {  // ~17 s at 2 GHz: a peer is gone
+        atomicExch(err, 1);
+        if (sum_newv) info->newv = 0;
+        return;
+      }
+    }
+    ull v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(&local[p].val) : "memory");
+    total += v;
+  }
+  if (sum_newv) info->newv = total;
+}
+
+cudaError_t launch_xbarrier(XSig* local, XSig* const* peers, int nranks, int me, ull* epoch_ctr, LevelInfo* info,
+                            bool sum_newv, int* err, cudaStream_t s) {
+  k_xbarrier<<<1, 32, 0, s>>>(local, peers, nranks, me, epoch_ctr, info, sum_newv ? 1 : 0, err);
+  return cudaGetLastError();
+}
+
+// the root's frontier bit in the all-gathered bitmap of a column peer of its owner (what the
+// first expand exchange would deliver)
+__global__ void k_seed_col(uint32_t* all_front, const uint32_t* perm_fwd, uint64_t root, uint64_t block, int i_owner) {
+  const uint64_t t = (uint64_t)perm_fwd[root] - (root / block) * block;
+  const uint64_t col_local = (uint64_t)i_owner * block + t;
+  all_front[col_local >> 5] |= 1u << (col_local & 31);
+}
+
+cudaError_t launch_seed_col(uint32_t* all_front, const uint32_t* perm_fwd, uint64_t root, uint64_t block, int i_owner,
+                            cudaStream_t s) {
+  k_seed_col<<<1, 1, 0, s>>>(all_front, perm_fwd, root, block, i_owner);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ list exchange
 // count of set bits of each of nseg segments of W words (grid.y = segment)
 __global__ void k_seg_popc(const uint32_t* __restrict__ bm, uint64_t W, ull* cnt) {

@@ -49,6 +49,13 @@ cudaError_t launch_list_encode(const uint32_t* bm, uint64_t W, int nseg, uint32_
 cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, cudaStream_t s);
 uint64_t list_kernel_launches();  // running count of the three launchers' kernels (process-wide)
 
+// Peer exchange (opts.peer_exchange): cross-GPU flag barrier over NVLink peer memory (optionally
+// summing the ranks' new-vertex counts into info->newv), and the root bit for column peers.
+cudaError_t launch_xbarrier(XSig* local, XSig* const* peers, int nranks, int me, unsigned long long* epoch_ctr,
+                            LevelInfo* info, bool sum_newv, int* err, cudaStream_t s);
+cudaError_t launch_seed_col(uint32_t* all_front, const uint32_t* perm_fwd, uint64_t root, uint64_t block, int i_owner,
+                            cudaStream_t s);
+
 // m_comp: sum of tdeg over reached owned vertices into *out (device u64).
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, unsigned long long* out, cudaStream_t s);
 

@@ -42,9 +42,9 @@ def test_struct_layout_matches_header(L):
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(bfs_comm), sizeof(bfs_opts), sizeof(bfs_info), sizeof(bfs_stats),
          sizeof(bfs_level_record));
-  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
          offsetof(bfs_level_record, edges), offsetof(bfs_opts, exchange), offsetof(bfs_stats, list_messages),
-         offsetof(bfs_stats, kernel_launches));
+         offsetof(bfs_stats, kernel_launches), offsetof(bfs_opts, peer_exchange));
   return 0;
 }
 '''
@@ -58,7 +58,8 @@ int main(void) {
     assert sizes[:5] == [ctypes.sizeof(bfs.Comm), ctypes.sizeof(bfs.Opts), ctypes.sizeof(bfs.Info),
                          ctypes.sizeof(bfs.Stats), ctypes.sizeof(bfs.LevelRecord)]
     assert sizes[5:] == [bfs.Info.nout.offset, bfs.Stats.bytes_exchanged.offset, bfs.LevelRecord.edges.offset,
-                         bfs.Opts.exchange.offset, bfs.Stats.list_messages.offset, bfs.Stats.kernel_launches.offset]
+                         bfs.Opts.exchange.offset, bfs.Stats.list_messages.offset, bfs.Stats.kernel_launches.offset,
+                         bfs.Opts.peer_exchange.offset]
 
 
 def test_strerror_and_null_args(L):

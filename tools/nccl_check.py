@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--grid", default="")
     ap.add_argument("--device-gen", action="store_true", help="generate the slice on the GPU")
     ap.add_argument("--exchange", default="bitmap", choices=["bitmap", "list", "auto"])
+    ap.add_argument("--peer", action="store_true", help="NVLink peer-memory exchange (opts.peer_exchange)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -47,7 +48,7 @@ def main():
         uid.copy_(torch.tensor(list(bfs.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(uid, 0)
     comm = bfs.make_comm(rank, world, local, loopback=False, nccl_id=bytes(uid.cpu().tolist()))
-    g = bfs.Graph(s, d, n, R, C, comm=comm, opts=bfs.make_opts(edges_per_thread=4, exchange=a.exchange))
+    g = bfs.Graph(s, d, n, R, C, comm=comm, opts=bfs.make_opts(edges_per_thread=4, exchange=a.exchange, peer_exchange=a.peer))
     info = g.info
     roots, t = [], 0
     while len(roots) < a.roots:
