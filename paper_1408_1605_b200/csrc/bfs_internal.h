@@ -124,6 +124,8 @@ struct Rank {
   // peer exchange (opts.peer_exchange): device arrays of peer pointers, null when inactive
   uint32_t** fold_dst = nullptr;  // [C] recv of P_ic + j*W (null for c == j)
   uint32_t** exp_dst = nullptr;   // [R] all_front of P_(i2)j + i*W (null for i2 == i)
+  uint32_t** reqin_dst = nullptr;   // [C] reqin of P_ic + j*W (null for c == j)
+  uint32_t** respin_dst = nullptr;  // [C] respin of P_ic + j*block (null for c == j)
   unsigned long long* scratch = nullptr;  // small reduction scratch
 };
 

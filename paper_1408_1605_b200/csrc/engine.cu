@@ -391,46 +391,59 @@ static int setup_peer(Graph& G) {
   CKR(cudaMemset(G.d_epoch, 0, 8));
   if ((rc = G_alloc(G, (void**)&G.d_xerr, 8))) return rc;
   CKR(cudaMemset(G.d_xerr, 0, 8));
-  if (!rk.recv) {  // C == 1: no fold buffer; a dummy keeps the handle layout uniform
-    if ((rc = G_alloc(G, (void**)&rk.recv, 16))) return rc;
-  }
-  cudaIpcMemHandle_t mine[3];
+  // C == 1: no fold / resolution buffers; dummies keep the handle layout uniform
+  if (!rk.recv && (rc = G_alloc(G, (void**)&rk.recv, 16))) return rc;
+  if (!rk.reqin && (rc = G_alloc(G, (void**)&rk.reqin, 16))) return rc;
+  if (!rk.respin && (rc = G_alloc(G, (void**)&rk.respin, 16))) return rc;
+  constexpr int NH = 5;
+  cudaIpcMemHandle_t mine[NH];
   CKR(cudaIpcGetMemHandle(&mine[0], rk.recv));
   CKR(cudaIpcGetMemHandle(&mine[1], rk.all_front));
   CKR(cudaIpcGetMemHandle(&mine[2], G.xsig));
+  CKR(cudaIpcGetMemHandle(&mine[3], rk.reqin));
+  CKR(cudaIpcGetMemHandle(&mine[4], rk.respin));
   const size_t hb = sizeof(mine);
   unsigned char* dbuf = nullptr;
   CKR(cudaMalloc(&dbuf, hb * (P + 1)));
   CKR(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice));
   NKR(ncclAllGather(dbuf, dbuf + hb, hb, ncclUint8, G.world, s));
-  std::vector<cudaIpcMemHandle_t> all((size_t)P * 3);
+  std::vector<cudaIpcMemHandle_t> all((size_t)P * NH);
   CKR(cudaMemcpyAsync(all.data(), dbuf + hb, hb * P, cudaMemcpyDeviceToHost, s));
   CKR(cudaStreamSynchronize(s));
   cudaFree(dbuf);
-  std::vector<void*> recv_of(P), front_of(P), sig_of(P);
+  std::vector<std::vector<void*>> of(NH, std::vector<void*>(P));  // [buffer][rank]
   for (int p = 0; p < P; ++p) {
     if (p == me) {
-      recv_of[p] = rk.recv;
-      front_of[p] = rk.all_front;
-      sig_of[p] = G.xsig;
+      of[0][p] = rk.recv;
+      of[1][p] = rk.all_front;
+      of[2][p] = G.xsig;
+      of[3][p] = rk.reqin;
+      of[4][p] = rk.respin;
       continue;
     }
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < NH; ++k) {
       void* ptr = nullptr;
-      cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)p * 3 + k], cudaIpcMemLazyEnablePeerAccess);
+      cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)p * NH + k], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
         cudaGetLastError();
         return set_err(BFS_ECUDA, "peer_exchange: cudaIpcOpenMemHandle of rank %d failed: %s", p,
                        cudaGetErrorString(e));
       }
       G.ipc_opened.push_back(ptr);
-      (k == 0 ? recv_of : k == 1 ? front_of : sig_of)[p] = ptr;
+      of[k][p] = ptr;
     }
   }
+  const std::vector<void*>&recv_of = of[0], &front_of = of[1], &sig_of = of[2], &reqin_of = of[3],
+                            &respin_of = of[4];
   // tables: fold_dst[c] = recv of P_ic + j*W; exp_dst[i2] = all_front of P_(i2)j + i*W
-  std::vector<uint32_t*> fold((size_t)g.C, nullptr), expd((size_t)g.R, nullptr);
+  std::vector<uint32_t*> fold((size_t)g.C, nullptr), expd((size_t)g.R, nullptr), rqd((size_t)g.C, nullptr),
+      rsd((size_t)g.C, nullptr);
   for (int c = 0; c < g.C; ++c)
-    if (c != rk.j) fold[c] = static_cast<uint32_t*>(recv_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
+    if (c != rk.j) {
+      fold[c] = static_cast<uint32_t*>(recv_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
+      rqd[c] = static_cast<uint32_t*>(reqin_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
+      rsd[c] = static_cast<uint32_t*>(respin_of[c * g.R + rk.i]) + (uint64_t)rk.j * g.block;
+    }
   for (int i2 = 0; i2 < g.R; ++i2)
     if (i2 != rk.i) expd[i2] = static_cast<uint32_t*>(front_of[rk.j * g.R + i2]) + (uint64_t)rk.i * W;
   std::vector<XSig*> sigs(P);
@@ -440,6 +453,10 @@ static int setup_peer(Graph& G) {
   if ((rc = G_alloc(G, (void**)&G.d_sig_peers, P * sizeof(XSig*)))) return rc;
   CKR(cudaMemcpy(rk.fold_dst, fold.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
   CKR(cudaMemcpy(rk.exp_dst, expd.data(), g.R * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  if ((rc = G_alloc(G, (void**)&rk.reqin_dst, g.C * sizeof(uint32_t*)))) return rc;
+  if ((rc = G_alloc(G, (void**)&rk.respin_dst, g.C * sizeof(uint32_t*)))) return rc;
+  CKR(cudaMemcpy(rk.reqin_dst, rqd.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  CKR(cudaMemcpy(rk.respin_dst, rsd.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
   CKR(cudaMemcpy(G.d_sig_peers, sigs.data(), P * sizeof(XSig*), cudaMemcpyHostToDevice));
   // the peers' arrays must be zero (epochs start at 0) before anyone signals
   NKR(ncclAllReduce(G.d_xerr, G.d_xerr, 1, ncclInt, ncclSum, G.world, s));
@@ -642,6 +659,17 @@ static int resolve_parents(Graph& G) {
   const uint64_t W = g.words_block();
   const int C = g.C;
   cudaStream_t s = G.stream;
+  if (peer_active(G)) {  // NEXT-2: requests and answers as peer stores, no host round trip
+    Rank& rk = G.ranks[0];
+    CKR(launch_req_build(g, rk, s));
+    CKR(launch_req_push(g, rk, s));
+    CKR(launch_popc_scan(rk.req, rk.off_req, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
+    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, false, G.d_xerr, s));
+    CKR(launch_popc_scan(rk.reqin, rk.off_in, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
+    CKR(launch_resp_push(g, rk, s));
+    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, false, G.d_xerr, s));
+    return BFS_OK;
+  }
   for (Rank& rk : G.ranks) CKR(launch_req_build(g, rk, s));
   // requests: rank (i,j) sends req segment c to (i,c), which stores it as reqin segment j
   if (G.world_size == 1) {
@@ -880,6 +908,14 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDefault, s));
   }
   CKR(cudaStreamSynchronize(s));
+  if (peer_active(G)) {  // the resolution's barriers
+    int xerr = 0;
+    CKR(cudaMemcpy(&xerr, G.d_xerr, sizeof(int), cudaMemcpyDeviceToHost));
+    if (xerr) {
+      G.broken = true;
+      return set_err(BFS_ENCCL, "peer_exchange: a cross-GPU barrier timed out (a peer stopped)");
+    }
+  }
   // per-level statistics of the device-side loop
   CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
   CKR(cudaStreamSynchronize(s));
@@ -917,7 +953,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     const bool peer = peer_active(G);
     const int owner_j = (int)(owner / (uint64_t)g.R);
     stats->kernel_launches =
-        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * 4 : 0) +
+        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
         (list_kernel_launches() - xk0) +
         (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
   }

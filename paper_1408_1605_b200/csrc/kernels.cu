@@ -1442,6 +1442,48 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Peer exchange of the resolution (no host round trip): the requester stores its request segment
+// c into P_ic's reqin (segment j); the responder stores each answer straight into the
+// requester's respin at the position the requester computes from its own request bitmap.
+__global__ void k_req_push(const uint32_t* req, uint32_t* const* __restrict__ dst, uint64_t W, int C) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < W * (uint64_t)C) {
+    const uint64_t c = gid / W;
+    if (dst[c]) dst[c][gid - c * W] = req[gid];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s) {
+  const uint64_t n = g.words_block() * g.C;
+  k_req_push<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.req, rk.reqin_dst, g.words_block(), g.C);
+  return cudaGetLastError();
+}
+
+// the packed answers of segment c (count from the request scan) copied to P_ic in 16-B stores
+__global__ void k_resp_copy(const uint32_t* resp, const uint32_t* off, uint32_t* const* __restrict__ dst, uint64_t W,
+                            uint64_t block, int C, int j) {
+  for (int c = 0; c < C; ++c) {
+    if (c == j || !dst[c]) continue;
+    const uint64_t n = off[(uint64_t)(c + 1) * W] - off[(uint64_t)c * W];
+    const uint4* src = reinterpret_cast<const uint4*>(resp + (uint64_t)c * block);
+    uint4* d = reinterpret_cast<uint4*>(dst[c]);
+    const uint64_t n4 = (n + 3) / 4;  // block is a multiple of 4: the padded tail stays in range
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * blockDim.x)
+      d[t] = src[t];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s) {
+  cudaError_t e = launch_resp_pack(g, rk, s);  // packed locally (coalesced), then one bulk copy per peer
+  if (e != cudaSuccess) return e;
+  k_resp_copy<<<num_sms() * 4, 256, 0, s>>>(rk.resp, rk.off_in, rk.respin_dst, g.words_block(), g.block, g.C, rk.j);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ m_comp, degree
 __global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uint32_t* tdeg, const uint32_t* fwd_own,
                                                uint64_t block, ull* out) {

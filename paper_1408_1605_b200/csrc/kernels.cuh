@@ -36,6 +36,9 @@ cudaError_t launch_popc_scan(const uint32_t* bits, uint32_t* off, uint64_t nword
                              cudaStream_t s);
 size_t popc_scan_tmp_bytes(uint64_t nwords);
 cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s);
+// peer exchange variants (stores into the peers' reqin / respin through rk.reqin_dst / respin_dst)
+cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s);
+cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s);
 
 cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s);
 
