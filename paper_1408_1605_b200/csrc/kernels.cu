@@ -1183,62 +1183,65 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
                                                 int j, const LevelCtrl* ctrl, uint32_t* const* __restrict__ exp_dst,
                                                 int R) {
-  // grid: x over the words of one segment, y = segment m (no 64-bit division)
+  // grid: x strides over the words of one segment (one pass unless the grid is capped), y = segment m
   const int lvl = (int)ctrl->lvl;  // the level being assigned (device-side: the loop may be a graph)
   const int m = (int)blockIdx.y;
   const int lane = threadIdx.x & 31;
-  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t gid = (uint64_t)m * W + w;
-  uint32_t newbits = 0;
-  uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
-  if (m == j && w < W) {
-    const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
-    const uint32_t vis = p.x;
-    uint32_t claimed = 0;
-    for (int c = 0; c < C; ++c) {
-      const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
-      if (c < 8) wbits[c] = x;
-      if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
-        uint32_t b = x;
-        while (b) {
-          const int bit = __ffs(b) - 1;
-          b &= b - 1;
-          winner[w * 32 + bit] = (uint8_t)c;
+  unsigned cnt = 0;
+  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x; wb < W; wb += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = wb + threadIdx.x;
+    const uint64_t gid = (uint64_t)m * W + w;
+    uint32_t newbits = 0;
+    uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
+    if (m == j && w < W) {
+      const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
+      const uint32_t vis = p.x;
+      uint32_t claimed = 0;
+      for (int c = 0; c < C; ++c) {
+        const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
+        if (c < 8) wbits[c] = x;
+        if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
+          uint32_t b = x;
+          while (b) {
+            const int bit = __ffs(b) - 1;
+            b &= b - 1;
+            winner[w * 32 + bit] = (uint8_t)c;
+          }
+        }
+        claimed |= x;
+      }
+      newbits = claimed;
+      if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
+      front_seg[w] = newbits;
+      if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
+        for (int i2 = 0; i2 < R; ++i2)
+          if (exp_dst[i2]) exp_dst[i2][w] = newbits;
+    } else if (w < W) {
+      const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
+      if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
+    }
+    // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing vertex
+    // 32k + l of word k (coalesced stores instead of per-bit scattered ones)
+    if (m == j) {
+      const uint64_t wbase = w - lane;
+      unsigned nz = __ballot_sync(0xFFFFFFFFu, newbits != 0);
+      while (nz) {
+        const int k = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t nb = __shfl_sync(0xFFFFFFFFu, newbits, k);
+        const uint64_t v = (wbase + k) * 32 + lane;
+        if ((nb >> lane) & 1u) level[v] = lvl;
+        if (winner) {
+          const int cmax = C < 8 ? C : 8;
+          for (int c = 0; c < cmax; ++c) {
+            const uint32_t x = __shfl_sync(0xFFFFFFFFu, wbits[c], k);
+            if ((x >> lane) & 1u) winner[v] = (uint8_t)c;
+          }
         }
       }
-      claimed |= x;
     }
-    newbits = claimed;
-    if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
-    front_seg[w] = newbits;
-    if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
-      for (int i2 = 0; i2 < R; ++i2)
-        if (exp_dst[i2]) exp_dst[i2][w] = newbits;
-  } else if (w < W) {
-    const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
-    if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
+    cnt += __popc(newbits);
   }
-  // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing vertex
-  // 32k + l of word k (coalesced stores instead of per-bit scattered ones)
-  if (m == j) {
-    const uint64_t wbase = w - lane;
-    unsigned nz = __ballot_sync(0xFFFFFFFFu, newbits != 0);
-    while (nz) {
-      const int k = __ffs(nz) - 1;
-      nz &= nz - 1;
-      const uint32_t nb = __shfl_sync(0xFFFFFFFFu, newbits, k);
-      const uint64_t v = (wbase + k) * 32 + lane;
-      if ((nb >> lane) & 1u) level[v] = lvl;
-      if (winner) {
-        const int cmax = C < 8 ? C : 8;
-        for (int c = 0; c < cmax; ++c) {
-          const uint32_t x = __shfl_sync(0xFFFFFFFFu, wbits[c], k);
-          if ((x >> lane) & 1u) winner[v] = (uint8_t)c;
-        }
-      }
-    }
-  }
-  unsigned cnt = __popc(newbits);
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&info->newv, (ull)cnt);
@@ -1250,7 +1253,11 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
 
 cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s) {
   const uint64_t W = g.words_block();
-  const dim3 grid((unsigned)((W + 255) / 256), (unsigned)g.C);
+  uint64_t gx = (W + 255) / 256;
+  // peer stores: each CTA ends with a system-scope fence, so a capped grid strides instead
+  const uint64_t cap = (uint64_t)num_sms() * 8 / (uint64_t)g.C;
+  if (g.R > 1 && rk.exp_dst && gx > cap) gx = cap ? cap : 1;
+  const dim3 grid((unsigned)gx, (unsigned)g.C);
   k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
                                 g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, ctrl,
                                 g.R > 1 ? rk.exp_dst : nullptr, g.R);
@@ -1446,8 +1453,8 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s) {
 // c into P_ic's reqin (segment j); the responder stores each answer straight into the
 // requester's respin at the position the requester computes from its own request bitmap.
 __global__ void k_req_push(const uint32_t* req, uint32_t* const* __restrict__ dst, uint64_t W, int C) {
-  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid < W * (uint64_t)C) {
+  for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < W * (uint64_t)C;
+       gid += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t c = gid / W;
     if (dst[c]) dst[c][gid - c * W] = req[gid];
   }
@@ -1457,7 +1464,8 @@ __global__ void k_req_push(const uint32_t* req, uint32_t* const* __restrict__ ds
 
 cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t n = g.words_block() * g.C;
-  k_req_push<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rk.req, rk.reqin_dst, g.words_block(), g.C);
+  const uint64_t blocks = (n + 255) / 256, cap = (uint64_t)num_sms() * 8;
+  k_req_push<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(rk.req, rk.reqin_dst, g.words_block(), g.C);
   return cudaGetLastError();
 }
 
