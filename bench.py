@@ -190,6 +190,14 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        return max_over_ranks_dist(x, world, dev)
+
     cfg = workload_config(args, world)
     scale = cfg["scale"]
     R, C = grid_of(args, world)
@@ -198,7 +206,12 @@ def run_ours(args, rank, world, local_rank):
     # this rank's slice of the tuple list, generated in HBM
     k0 = M * rank // world
     k1 = M * (rank + 1) // world
+    torch.cuda.synchronize()
+    barrier()
+    t_gen = time.perf_counter()
     ds, dd = inputs.generate_device(scale, k0=k0, count=k1 - k0, device=dev)
+    torch.cuda.synchronize()
+    t_gen = max_over_ranks(time.perf_counter() - t_gen)
     stream = torch.cuda.current_stream(dev)
     # timed steps: the level loop runs as one CUDA graph (no phase events); the per-phase CUDA-event
     # times (roofline of the expansion kernel) come from a replay of the same roots afterwards
@@ -215,9 +228,10 @@ def run_ours(args, rank, world, local_rank):
     else:
         comm = bfs.make_comm(0, 1, local_rank, loopback=True)
     torch.cuda.synchronize()
+    barrier()
     t_build = time.perf_counter()
-    g = bfs.Graph(ds, dd, n, R, C, comm=comm, opts=opts)
-    t_build = time.perf_counter() - t_build
+    g = bfs.Graph(ds, dd, n, R, C, comm=comm, opts=opts)  # returns after the graph is resident
+    t_build = max_over_ranks(time.perf_counter() - t_build)
     del ds, dd
     torch.cuda.empty_cache()
     info = g.info
@@ -230,13 +244,6 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        return max_over_ranks_dist(x, world, dev)
 
     for k in range(args.warmup):
         g.run(warm_roots[k % len(warm_roots)], parent, level)
@@ -350,6 +357,10 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
         "graph": {"nverts": n, "tuples": M, "nnz_rank0": int(info.nnz_local), "build_s": t_build,
                   "device_bytes_rank0": int(info.device_bytes)},
+        # Graph500 kernel 1 (§8(f) NEXT-3): tuple generation in HBM + partition/shuffle/CSC+CSR
+        # build, wall clock, max over ranks
+        "construction": {"generate_s": t_gen, "build_s": t_build,
+                         "tuples_per_s": M / (t_gen + t_build) if t_gen + t_build > 0 else None},
     }
     if world == 1 and not args.no_cpu_baseline:
         ns = int(os.environ.get("BENCH_CPU_ROOTS", "4"))
