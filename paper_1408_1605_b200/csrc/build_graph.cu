@@ -124,6 +124,16 @@ __global__ void k_iota2(uint32_t* a, uint32_t* b, uint64_t n) {
     a[v] = b[v] = (uint32_t)v;
 }
 
+// full per-block degree sort: relabeled id k <- vertex sorted[k] (blocks stay in place: the sort
+// key starts with the block)
+__global__ void k_perm_from_sorted(const uint32_t* sorted, uint64_t n, uint32_t* fwd, uint32_t* inv) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = sorted[k];
+    fwd[v] = (uint32_t)k;
+    inv[k] = v;
+  }
+}
+
 __global__ void k_apply_moves(const uint32_t* moves, uint64_t nmoves, uint32_t* fwd, uint32_t* inv) {
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nmoves; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t o = moves[2 * t], n = moves[2 * t + 1];
@@ -207,6 +217,12 @@ static int compute_relabel(Graph& G, const uint32_t* sdeg, uint32_t* fwd, uint32
   k_degree_keys<<<4096, 256, 0, s>>>(sdeg, g.npad, g.block, keys, vals);
   CKR(cudaGetLastError());
   CKR(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (uint64_t)g.npad, 0, kb, s));
+  if (H >= g.block) {  // the whole block in degree order: position k holds vertex vals2[k]
+    k_perm_from_sorted<<<4096, 256, 0, s>>>(vals2, g.npad, fwd, inv);
+    CKR(cudaGetLastError());
+    CKR(cudaStreamSynchronize(s));
+    return BFS_OK;
+  }
   std::vector<uint32_t> hot(P * H);
   for (uint64_t b = 0; b < P; ++b)
     CKR(cudaMemcpyAsync(hot.data() + b * H, vals2 + b * g.block, H * 4, cudaMemcpyDeviceToHost, s));

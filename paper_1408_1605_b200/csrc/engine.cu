@@ -304,9 +304,10 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   G.g.R = R;
   G.g.C = C;
   G.g.block = G.g.npad / P;
-  {  // degree-ordered prefix per vertex block; BFS200_HOT_PREFIX overrides (experiments)
+  {  // degree-ordered prefix per vertex block: by default the whole block (a full
+     // degree sort); BFS200_HOT_PREFIX sets a shorter prefix (experiments)
     const char* env = getenv("BFS200_HOT_PREFIX");
-    const uint64_t want = (env && atoll(env) > 0) ? (uint64_t)atoll(env) : (1ull << 22);
+    const uint64_t want = (env && atoll(env) > 0) ? (uint64_t)atoll(env) : ~0ull;
     G.hot_h = G.g.block < want ? G.g.block : want;
     G.hot_h &= ~31ull;
     if (!G.hot_h) G.hot_h = G.g.block;
