@@ -295,7 +295,8 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   } else {
     rk.nnz = 0;
   }
-  rc = G_alloc(G, (void**)&rk.row, (rk.nnz ? rk.nnz : 1) * sizeof(uint32_t));
+  // + 4 entries: K1's bulk copies round a tile's byte range out to 16-B boundaries
+  rc = G_alloc(G, (void**)&rk.row, (rk.nnz + 4) * sizeof(uint32_t));
   if (rc) return rc;
   rc = G_alloc(G, (void**)&rk.col, (g.ncols() + 1) * sizeof(ull));
   if (rc) return rc;

@@ -72,6 +72,43 @@ __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
                ::"l"(a), "r"(m), "r"((int)p));
 }
 
+// mbarrier + 1D bulk copy (TMA engine, UBLKCP): global -> shared without registers or L1
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint32_t bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+#ifndef BFS200_RING_EF
+#define BFS200_RING_EF 0
+#endif
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+#if BFS200_RING_EF
+  // streamed once: evict-first in L2, so the visited/discovered lines stay resident
+  asm volatile(
+      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+#else
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+#endif
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT;\n"
+      "}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -498,6 +535,35 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
 constexpr size_t kSmemTarget = 160 * 1024;  // K1 dynamic shared memory (staging + hot copy)
+// Long-column tiles of a P2 level in flight per warp: their `row` entries are fetched by 1D bulk
+// copies (cp.async.bulk, TMA engine) into a per-warp shared-memory ring, so the bytes in flight
+// are bounded by the ring, not by registers or L1 capacity.  0 = register loads (double-buffered).
+#ifndef BFS200_RING
+#define BFS200_RING 0
+#endif
+constexpr int kRing = BFS200_RING;
+#ifndef BFS200_DEFER
+#define BFS200_DEFER 0
+#endif
+constexpr bool kDefer = BFS200_DEFER;  // ring loop: a tile's REDs after the next tile's probes
+// per-warp ring: kRing mbarriers (padded to 16 B), then kRing slots of TILE + 4 words (a tile's
+// range rounded out to 16-B boundaries: up to 3 leading words)
+template <int E>
+__host__ __device__ constexpr size_t ring_bytes_per_warp() {
+  return kRing ? 16 * ((kRing * 8 + 15) / 16) + (size_t)kRing * (32 * E + 4) * 4 : 0;
+}
+// per-warp chunk before the hot-copy region: the warp's short-tile staging (s_off, s_beg) and its
+// long-tile ring overlay each other (a warp finishes its long tiles before it stages short ones)
+template <int E>
+__host__ __device__ constexpr size_t expand_warp_bytes(bool pos32) {
+  return 16 * (((32 * E + 2) * ((pos32 ? 4 : 8) + 4) > ring_bytes_per_warp<E>()
+                    ? ((32 * E + 2) * ((pos32 ? 4 : 8) + 4) + 15) / 16
+                    : (ring_bytes_per_warp<E>() + 15) / 16));
+}
+template <int E, int THREADS>
+__host__ __device__ constexpr size_t expand_stage_bytes(bool pos32) {
+  return (THREADS / 32) * expand_warp_bytes<E>(pos32);
+}
 
 // Visited word of row v in the shared-memory hot copy.  Layout: per row segment hw words of the
 // hot prefix and one zero sentinel (word hw), so rows past the prefix need no range test: their
@@ -582,6 +648,23 @@ __device__ __forceinline__ void probe_red(const Probe& p) {
                "}" ::"r"(p.x), "r"(p.y), "r"(p.m), "r"(p.need), "l"(p.a));
 }
 
+// Deferred form of probe_red for a row v whose probe result (x, y, need) was kept in registers
+// (the ring loop issues the next tile's probes before this RED; the bit is idempotent).
+__device__ __forceinline__ void red_deferred(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
+  asm volatile("{\n"
+               " .reg .pred pn, pr;\n"
+               " .reg .b32 t, m;\n"
+               " .reg .b64 a;\n"
+               " setp.ne.b32 pn, %3, 0;\n"
+               " shf.l.wrap.b32 m, 0, 1, %0;\n"
+               " lop3.b32 t, %1, %2, m, 0xa8;\n"
+               " setp.eq.and.b32 pr, t, 0, pn;\n"
+               " shr.b32 t, %0, 5;\n"
+               " mad.wide.u32 a, t, 8, %4;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
+               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
+}
+
 // One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
 // against the shared-memory copy, the others with one 8-byte load of the visited|discovered
 // pair), then the discovered bit by RED.OR and, in P1 levels, the parent claim.
@@ -632,10 +715,11 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   // staged row positions: 32-bit when every CSC position fits (nnz < 2^32; modular arithmetic
   // below stays exact), which leaves more of the SM's unified L1/shared memory to L1
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
-  Pos* s_off = reinterpret_cast<Pos*>(smem) + wid * SLOT;
-  uint32_t* s_beg = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + wid * SLOT;
+  unsigned char* wchunk = smem + (size_t)wid * expand_warp_bytes<E>(POS32);
+  Pos* s_off = reinterpret_cast<Pos*>(wchunk);
+  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_off + SLOT);
   // the region after the staging holds either the parents' ids (P1) or the hot visited bits
-  uint32_t* s_region = reinterpret_cast<uint32_t*>(reinterpret_cast<Pos*>(smem) + WARPS * SLOT) + WARPS * SLOT;
+  uint32_t* s_region = reinterpret_cast<uint32_t*>(smem + expand_stage_bytes<E, THREADS>(POS32));
   // P1: the per-warp parents' ids sit at the end of the region, the hot copy (P2, mode 3) at its start
   uint32_t* s_u = s_region + (region_words - WARPS * SLOT) + wid * SLOT;
   const uint32_t* s_hot = s_region;
@@ -703,6 +787,91 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       }
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
+    if constexpr (!P1 && kRing > 0) {
+      // ring of kRing bulk-copied tiles per warp; slot s holds tiles t + (kRing*k + s)*stride
+      constexpr uint32_t SW = TILE + 4;  // slot words
+      constexpr uint32_t BARB = 16 * ((kRing * 8 + 15) / 16);
+      unsigned char* wring = wchunk;
+      const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(wring);
+      const uint32_t slot0 = bar0 + BARB;
+      const uint32_t* slots = reinterpret_cast<const uint32_t*>(wring + BARB);
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kRing; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // inits visible to the copy engine
+      }
+      __syncwarp();
+      uint32_t ro[kRing], rl[kRing];  // per slot: leading words, tile length
+      ull ti = t;                     // next tile to issue, its record already loaded
+      uint4 nrec = ti < nA ? tileA[ti] : make_uint4(0, 0, 0, 0);
+      auto issue = [&](const int s) {
+        const ull pos = (ull)nrec.x | ((ull)nrec.y << 32);
+        const uint32_t o = (uint32_t)pos & 3u;
+        ro[s] = o;
+        rl[s] = nrec.z;
+        if (lane == 0)
+          bulk_g2s(slot0 + s * SW * 4, row + (pos - o), ((o + nrec.z) * 4u + 15u) & ~15u, bar0 + 8 * s);
+        ti += stride;
+        nrec = ti < nA ? tileA[ti] : make_uint4(0, 0, 0, 0);
+      };
+#pragma unroll
+      for (int s = 0; s < kRing; ++s)
+        if (ti < nA) issue(s);
+      uint32_t parity = 0;
+      uint32_t pv[E], px[E], py[E], pn[E];  // kDefer: the previous tile's rows and probe results
+      bool have = false;
+      while (t < nA) {
+#pragma unroll
+        for (int s = 0; s < kRing; ++s) {
+          if (t + (ull)s * stride < nA) {  // warp-uniform
+            mbar_wait(bar0 + 8 * s, parity);
+            uint32_t v[E];
+            const uint32_t* sp = slots + s * SW + ro[s] + lane;
+#pragma unroll
+            for (int q = 0; q < E; ++q) v[q] = sp[32 * q];  // Alg.3 line 4 (lanes past len: unused)
+            const uint32_t len = rl[s];
+            __syncwarp();  // every lane has read the slot: refill it
+            if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (ti < nA) issue(s);
+            Probe pr[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {  // Alg.3 lines 5-6
+              if (SEG1) probe_seg1(pr[q], v[q], 32u * q + lane, len, hw, sa, vd);
+              else probe_segs(pr[q], v[q], 32u * q + lane, len, hw, sa, vd, bl, bmask);
+            }
+            if (kDefer) {  // the previous tile's REDs while this tile's probes are in flight
+              if (have) {
+#pragma unroll
+                for (int q = 0; q < E; ++q) red_deferred(pv[q], px[q], py[q], pn[q], vd);
+              }
+#pragma unroll
+              for (int q = 0; q < E; ++q) {
+                pv[q] = v[q];
+                px[q] = pr[q].x;
+                py[q] = pr[q].y;
+                pn[q] = pr[q].need;
+              }
+              have = true;
+            } else {
+#pragma unroll
+              for (int q = 0; q < E; ++q) probe_red(pr[q]);  // Alg.3 line 7
+            }
+          }
+        }
+        parity ^= 1u;
+        t += (ull)kRing * stride;
+      }
+      if (kDefer && have) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) red_deferred(pv[q], px[q], py[q], pn[q], vd);
+      }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kRing; ++s) mbar_inval(bar0 + 8 * s);
+      }
+      __syncwarp();  // the ring's memory is the short tiles' staging next
+    } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;
     uint4 rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
@@ -737,6 +906,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         t1 = t + stride;
         rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
       }
+    }
     }
   }
   // ---- short columns: tiles of TILE consecutive short edges, scan + binary-search mapping
@@ -914,7 +1084,7 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   constexpr int SLOT = 32 * E + 2;
   constexpr size_t WARPS = THREADS / 32;
   const bool pos32 = rk.nnz < (1ull << 32);  // every CSC position fits in 32 bits
-  const size_t staging = WARPS * SLOT * ((pos32 ? 4 : 8) + 4);
+  const size_t staging = expand_stage_bytes<E, THREADS>(pos32);
   const size_t s_u_bytes = WARPS * SLOT * 4;
   // hot visited words per row segment: the relabeled prefix, as far as shared memory allows
   int blog = -1;
