@@ -34,7 +34,9 @@ struct LevelInfo {
   unsigned long long ncols;   // short columns (stats)
   unsigned long long nlongcols;  // long columns (stats)
   unsigned long long disc_total;  // rows discovered by this rank so far in this search (K4 counts)
-  unsigned long long pad[6];
+  unsigned long long blind;   // mode 3 with few rows visited: claims without the visited probe
+                              // for rows past the hot prefix (K4 masks the visited rows)
+  unsigned long long pad[5];
 };
 
 // One slot of the peer-exchange signal array (one slot per sending rank).

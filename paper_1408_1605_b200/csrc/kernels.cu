@@ -259,6 +259,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   if (lane == 0) seg_tot[seg] = t;
 }
 
+#ifndef BFS200_BLIND3
+#define BFS200_BLIND3 1
+#endif
+constexpr bool kBlind3 = BFS200_BLIND3;
+
 // level totals from the segment scan (seg_off[nseg] = sum over all segments); resets counters
 __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* info, ull* cumul, ull nnz,
                              ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
@@ -282,6 +287,9 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   // pass derives the discovered words from pmin in one pass over the rows (cheaper than a
   // RED.OR and a probe per edge once edges * m3_factor >= rows)
   if (info->mode == 1 && m3_factor && edges * m3_factor >= nrows) info->mode = 3ull;
+  // mode 3 while at most 1/16 of the rows are visited (the first dense level): the visited
+  // probe of a non-hot row almost never finds the bit set, so the claim goes out without it
+  info->blind = (info->mode == 3 && kBlind3 && seen * 16ull <= nz_rows) ? 1ull : 0ull;
   info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
   info->nlongcols = 0;
   cumul[c.cs] = c.ss;
@@ -674,7 +682,7 @@ __device__ __forceinline__ void red_deferred(uint32_t v, uint32_t x, uint32_t y,
 template <int WV, bool P1, bool SEG1>
 __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vd,
                                              uint32_t* pmin, const uint32_t* s_hot, uint32_t bmask, int bl,
-                                             uint32_t hw, bool claim3 = false) {
+                                             uint32_t hw, bool claim3 = false, bool blind3 = false) {
   uint32_t wx[WV], wy[WV];
   bool need[WV], probe[WV];
 #pragma unroll
@@ -686,7 +694,8 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
     if (!P1 || claim3) {
       need[q] = ok && !(hot_word<SEG1>(s_hot, v[q], ok, hw, bl, bmask) & m);
       const uint32_t off = SEG1 ? v[q] : (v[q] & bmask);
-      probe[q] = need[q] && !(claim3 && off < hw * 32u);  // claim3: hot rows are decided already
+      // claim3: hot rows are decided already; blind3: the other rows claim without a probe
+      probe[q] = need[q] && !(claim3 && (blind3 || off < hw * 32u));
     }
     ld_cg_u2_p(probe[q], vd + 2 * (v[q] >> 5), wx[q], wy[q]);
   }
@@ -705,7 +714,8 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
                                             ull nA, ull n, ull total, ull all_edges, uint32_t* vd, uint32_t* pmin,
                                             const uint32_t* __restrict__ inv_col, uint32_t hot_words, int C,
-                                            uint64_t W, int blog, uint32_t region_words, bool claim3) {
+                                            uint64_t W, int blog, uint32_t region_words, bool claim3,
+                                            bool blind3) {
   constexpr int TILE = 32 * E;
   constexpr int WARPS = THREADS / 32;
   constexpr int SLOT = TILE + 2;
@@ -773,7 +783,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           uint32_t ug[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
-          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
+          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
         } else {
           Probe pr[LWV];
 #pragma unroll
@@ -997,7 +1007,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = u0;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
       }
     } else {
       // lane-interleaved edges e = 32q + lane; lane state: the staged column idx holding its
@@ -1044,7 +1054,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = P1 ? s_u[idx] : 0u;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3);
+        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
       }
     }
     if (!rnext) {
@@ -1073,10 +1083,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
   if (all_edges == 0) return;
   if (info->mode != 2)
     expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd,
-                                               pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3);
+                                               pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3,
+                                               info->blind != 0);
   else
     expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges,
-                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false);
+                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false, false);
 }
 
 template <int E, int THREADS>
@@ -1170,7 +1181,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
   uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const bool p1 = info->mode == 1, m3 = info->mode == 3;
+  const bool p1 = info->mode == 1, m3 = info->mode == 3, blind = m3 && info->blind;
   unsigned ndisc = 0;
   // P2: frontier bits of the hot (relabeled, highest-degree) column prefix of each of the R
   // column segments, so most frontier tests of the CSR scans stay in shared memory
@@ -1196,16 +1207,18 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
       // the chunk's word k (coalesced), the ballot is word k's discovered bits
       uint32_t myd = 0;
       const int nk = (int)min((uint64_t)32, nwords - ch * 32);
+      // visited words of the chunk (blind claims may have reached visited rows: not discovered)
+      const uint32_t visw = (blind && w < nwords) ? vd[2 * w] : 0u;
 #pragma unroll 4
       for (int k = 0; k < nk; ++k) {
         const uint64_t r = (ch * 32 + k) * 32 + lane;
         const uint32_t pm = pmin[r];
-        const bool f = pm != 0xFFFFFFFFu;
+        const uint32_t vk = __shfl_sync(0xFFFFFFFFu, visw, k);
+        const bool c = pm != 0xFFFFFFFFu;
+        const bool f = c && !((vk >> lane) & 1u);
         const unsigned dd = __ballot_sync(0xFFFFFFFFu, f);
-        if (f) {
-          pred[r] = pm;
-          pmin[r] = 0xFFFFFFFFu;
-        }
+        if (f) pred[r] = pm;
+        if (c) pmin[r] = 0xFFFFFFFFu;
         if (lane == k) myd = dd;
       }
       if (w < nwords) {
