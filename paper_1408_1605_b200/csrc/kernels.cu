@@ -191,6 +191,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   SegTot t{0u, 0u, 0ull, 0ull};
+  {  // all words of the segment in one round trip; an empty segment (sparse levels) ends here
+    uint32_t any = 0;
+#pragma unroll
+    for (int c = 0; c < kScanSegWords / 32; ++c) {
+      const uint64_t w = w0 + 32 * c + lane;
+      any |= (w < w1) ? __ldg(bm + w) : 0u;
+    }
+    if (!__any_sync(0xFFFFFFFFu, any != 0u)) {
+      if (lane == 0) seg_tot[seg] = SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
+      return;
+    }
+  }
   __shared__ uint16_t s_lists[kScanThreads / 32][1024];
   uint16_t* s_list = s_lists[threadIdx.x >> 5];
   auto add_col = [&](ull d) {
@@ -317,6 +329,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const SegTot o = seg_off[seg];
+  {  // nothing to emit (no column of non-zero degree in the segment): skip the bitmap
+    const SegTot o1 = seg_off[seg + 1];
+    if (o1.cs == o.cs && o1.na == o.na) return;
+  }
   uint64_t k = o.cs;  // next short list position
   ull e = o.ss;       // next short edge position
   uint64_t a = o.na;  // next long-tile position
