@@ -1225,17 +1225,25 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
       const int nk = (int)min((uint64_t)32, nwords - ch * 32);
       // visited words of the chunk (blind claims may have reached visited rows: not discovered)
       const uint32_t visw = (blind && w < nwords) ? vd[2 * w] : 0u;
-#pragma unroll 4
-      for (int k = 0; k < nk; ++k) {
-        const uint64_t r = (ch * 32 + k) * 32 + lane;
-        const uint32_t pm = pmin[r];
-        const uint32_t vk = __shfl_sync(0xFFFFFFFFu, visw, k);
-        const bool c = pm != 0xFFFFFFFFu;
-        const bool f = c && !((vk >> lane) & 1u);
-        const unsigned dd = __ballot_sync(0xFFFFFFFFu, f);
-        if (f) pred[r] = pm;
-        if (c) pmin[r] = 0xFFFFFFFFu;
-        if (lane == k) myd = dd;
+      // 16 rows' pmin loads in flight per lane (a streaming pass: bytes in flight set its speed)
+#pragma unroll 1
+      for (int k0 = 0; k0 < nk; k0 += 16) {
+        uint32_t pm[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          pm[q] = (k0 + q < nk) ? pmin[(ch * 32 + k0 + q) * 32 + lane] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int k = k0 + q;
+          const uint64_t r = (ch * 32 + k) * 32 + lane;
+          const uint32_t vk = __shfl_sync(0xFFFFFFFFu, visw, k);
+          const bool c = pm[q] != 0xFFFFFFFFu;
+          const bool f = c && !((vk >> lane) & 1u);
+          const unsigned dd = __ballot_sync(0xFFFFFFFFu, f);
+          if (f) pred[r] = pm[q];
+          if (c) pmin[r] = 0xFFFFFFFFu;
+          if (lane == k) myd = dd;
+        }
       }
       if (w < nwords) {
         vd[2 * w + 1] = myd;
