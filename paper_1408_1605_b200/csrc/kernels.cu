@@ -1182,6 +1182,10 @@ constexpr int kShortScan = 32;
 #define BFS200_LANE_STEP 4
 #endif
 constexpr int kLaneStep = BFS200_LANE_STEP;  // CSR entries per lane step (loads in flight together)
+#ifndef BFS200_PAR_ROWS
+#define BFS200_PAR_ROWS 2
+#endif
+constexpr int kParRows = BFS200_PAR_ROWS;  // P2 rows scanned together per lane
 constexpr size_t kParentHotSmem = 64 * 1024;  // hot prefix of the frontier bitmap (P2 levels)
 
 __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint64_t nwords,
@@ -1293,29 +1297,57 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
     }
     __syncwarp();
     unsigned nlong = 0;  // lane-local count of deferred rows (written at slots lane, lane+32, ...)
-    for (unsigned q = lane; q < total; q += 32) {
-      const uint32_t r = queue[wid][q];
-      const ull beg = csr_ptr[r], end = csr_ptr[r + 1];
-      const ull stop = min(end, beg + kShortScan);
-      uint32_t best = 0xFFFFFFFFu;
-      ull p = beg;
-      for (; p < stop && best == 0xFFFFFFFFu; p += kLaneStep) {
-        uint32_t u[kLaneStep];
-        bool f[kLaneStep];
+    // kParRows rows per lane at a time: their dependent chains (row pointers -> first CSR entries
+    // -> frontier tests -> inv_col) overlap, so more random loads are in flight per lane
+    for (unsigned q0 = lane; q0 < total; q0 += 32 * kParRows) {
+      uint32_t r[kParRows], best[kParRows];
+      ull p[kParRows], stop[kParRows];
 #pragma unroll
-        for (int k = 0; k < kLaneStep; ++k) u[k] = (p + k < stop) ? __ldg(csr_col + p + k) : 0xFFFFFFFFu;
+      for (int i = 0; i < kParRows; ++i) r[i] = (q0 + 32 * i < total) ? queue[wid][q0 + 32 * i] : 0xFFFFFFFFu;
 #pragma unroll
-        for (int k = 0; k < kLaneStep; ++k)
-          f[k] = (u[k] != 0xFFFFFFFFu) && in_front(u[k]);
-#pragma unroll
-        for (int k = kLaneStep - 1; k >= 0; --k)
-          if (f[k]) best = u[k];
+      for (int i = 0; i < kParRows; ++i) {
+        const bool v = r[i] != 0xFFFFFFFFu;
+        const ull beg = v ? csr_ptr[r[i]] : 0ull, end = v ? csr_ptr[r[i] + 1] : 0ull;
+        p[i] = beg;
+        stop[i] = min(end, beg + kShortScan);
+        best[i] = 0xFFFFFFFFu;
       }
-      if (best != 0xFFFFFFFFu) {
-        pred[r] = inv_col[best];
-      } else {  // defer to the whole warp; slot lane+32*nlong <= q was already consumed
-        queue[wid][lane + 32 * nlong] = r;
-        ++nlong;
+      bool more = true;
+      while (more) {  // every row still searching takes one lane step, all rows' loads together
+        uint32_t u[kParRows][kLaneStep];
+#pragma unroll
+        for (int i = 0; i < kParRows; ++i) {
+          const bool act = best[i] == 0xFFFFFFFFu && p[i] < stop[i];
+#pragma unroll
+          for (int k = 0; k < kLaneStep; ++k)
+            u[i][k] = (act && p[i] + k < stop[i]) ? __ldg(csr_col + p[i] + k) : 0xFFFFFFFFu;
+        }
+        more = false;
+#pragma unroll
+        for (int i = 0; i < kParRows; ++i) {
+          bool f[kLaneStep];
+#pragma unroll
+          for (int k = 0; k < kLaneStep; ++k) f[k] = (u[i][k] != 0xFFFFFFFFu) && in_front(u[i][k]);
+#pragma unroll
+          for (int k = kLaneStep - 1; k >= 0; --k)
+            if (f[k]) best[i] = u[i][k];
+          p[i] += kLaneStep;
+          more |= best[i] == 0xFFFFFFFFu && p[i] < stop[i];
+        }
+      }
+      uint32_t pv[kParRows];
+#pragma unroll
+      for (int i = 0; i < kParRows; ++i)
+        pv[i] = (r[i] != 0xFFFFFFFFu && best[i] != 0xFFFFFFFFu) ? inv_col[best[i]] : 0u;
+#pragma unroll
+      for (int i = 0; i < kParRows; ++i) {
+        if (r[i] == 0xFFFFFFFFu) continue;
+        if (best[i] != 0xFFFFFFFFu) {
+          pred[r[i]] = pv[i];
+        } else {  // defer to the whole warp; slot lane+32*nlong <= q0+32i was already read
+          queue[wid][lane + 32 * nlong] = r[i];
+          ++nlong;
+        }
       }
     }
     __syncwarp();
