@@ -24,8 +24,9 @@
  *     on one GPU and the calls are ordinary.
  *   - A CUDA or NCCL failure is fatal for the graph: it returns BFS_ECUDA / BFS_ENCCL and
  *     every later call on that graph returns BFS_ESTATE.
- *   - No global mutable state besides the thread-local error string; distinct graphs may be
- *     used from distinct threads.
+ *   - No global mutable state besides the thread-local error string (launch attributes and SM
+ *     counts are set / read per graph on its own device); distinct graphs may be used from
+ *     distinct threads.  One graph must not be used from two threads at once.
  */
 #ifndef BFS200_H
 #define BFS200_H
@@ -85,8 +86,16 @@ typedef struct {
                            sums the new-vertex counts) replace the all-gather, the send/recv and
                            the all-reduce.  Needs CUDA IPC / peer access between the ranks' GPUs
                            (set up collectively on the first run) and exchange = 0; ignored by
-                           loopback and 1x1.  0 (default): NCCL collectives. */
+                           loopback and 1x1.  0 (default): NCCL collectives.  At the start of
+                           every bfs_run the ranks meet in one 4-byte NCCL all-reduce, so a rank
+                           may reach bfs_run arbitrarily long after its peers; within a run a peer
+                           that stops for ~17 s makes the run fail with BFS_ENCCL. */
+  int debug_flags;      /* testing only; 0 in production.  BFS_DEBUG_POS64: the expansion stages
+                           64-bit row positions even when every position fits in 32 bits (the
+                           kernel variant otherwise used only when a rank holds >= 2^32 entries). */
 } bfs_opts;
+
+enum { BFS_DEBUG_POS64 = 1 };
 
 enum { BFS_XCHG_BITMAP = 0, BFS_XCHG_LIST = 1, BFS_XCHG_AUTO = 2 };
 
@@ -175,8 +184,23 @@ int bfs_run(bfs_graph* g, uint64_t root, int64_t* parent, int32_t* level, bfs_st
 int bfs_mcomp(bfs_graph* g, uint64_t* m_comp);
 
 /* Per-level phase times of the last run (requires opts.phase_timing). Writes up to
- * max_levels records and the level count to *nlevels. Synchronises on the recorded events. */
+ * max_levels records and the number of recorded levels to *nlevels: every level of the run,
+ * except that records stop after the first 4096 levels (a deeper BFS, e.g. on a long path, runs
+ * to completion; bfs_stats.nlevels and its totals cover every level).  Synchronises on the
+ * recorded events. */
 int bfs_level_times(bfs_graph* g, bfs_level_record* out, int max_levels, int* nlevels);
+
+/* Gather the outputs of every rank on rank 0 (untimed, for validation).
+ * COLLECTIVE over the R*C ranks (NCCL point-to-point sends to world rank 0); with the loopback
+ * transport the process already holds every rank and the call is a copy.
+ *   parent, level        : this process's bfs_run outputs (info.nout entries each; host or
+ *                          device), or NULL to skip -- NULL-ness must agree on every rank.
+ *   parent_all, level_all: on world rank 0 only (ignored elsewhere, may be NULL there):
+ *                          info.npad entries each (host or device), entry t = global vertex t
+ *                          (rank r's slice lands at r*block; padding vertices are -1 / -1).
+ * Errors: BFS_EINVAL (rank 0 misses an output for a non-NULL input), BFS_ENOMEM, BFS_ECUDA,
+ * BFS_ENCCL (the latter two are fatal for the graph). */
+int bfs_gather(bfs_graph* g, const int64_t* parent, const int32_t* level, int64_t* parent_all, int32_t* level_all);
 
 /* NULL-safe, idempotent for NULL.  Collective with NCCL. */
 void bfs_destroy(bfs_graph* g);

@@ -26,7 +26,7 @@ V_NAMES = ["V1 root", "V2 tree-edge", "V3 level+1", "V4 edge-span", "V5 componen
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so with gcc (plain -O2, no vectorisation tricks needed)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -53,6 +53,14 @@ def lib():
         L.oracle_mcomp.restype = u64
         L.oracle_validate.argtypes = [u64, u64, p, p, u64, p, p]
         L.oracle_validate.restype = ctypes.c_int
+        L.oracle_vstream_begin.argtypes = [u64, u64, p, p]
+        L.oracle_vstream_begin.restype = p
+        L.oracle_vstream_feed.argtypes = [p, u64, p, p]
+        L.oracle_vstream_feed.restype = None
+        L.oracle_vstream_mcomp.argtypes = [p]
+        L.oracle_vstream_mcomp.restype = u64
+        L.oracle_vstream_end.argtypes = [p]
+        L.oracle_vstream_end.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -112,3 +120,24 @@ def validate(n: int, src, dst, root: int, level, parent) -> int:
 
 def failed_names(mask: int):
     return [V_NAMES[i] for i in range(len(V_NAMES)) if mask >> i & 1]
+
+
+def validate_stream(n: int, root: int, level, parent, chunks):
+    """Streaming V1..V6 (oracle.c step 6): `chunks` yields (src, dst) tuple arrays, e.g. the
+    tuple list regenerated from its seed chunk by chunk.  Returns (mask, m_comp)."""
+    level = np.ascontiguousarray(level, dtype=np.int32)
+    parent = np.ascontiguousarray(parent, dtype=np.int64)
+    if level.size < n or parent.size < n:
+        raise ValueError("level/parent shorter than n")
+    L = lib()
+    st = L.oracle_vstream_begin(int(n), int(root), level.ctypes.data, parent.ctypes.data)
+    if not st:
+        raise MemoryError("oracle_vstream_begin failed")
+    try:
+        for s, d in chunks:
+            s, d = _u64(s), _u64(d)
+            L.oracle_vstream_feed(st, int(s.size), s.ctypes.data, d.ctypes.data)
+        mc = int(L.oracle_vstream_mcomp(st))
+    finally:
+        mask = int(L.oracle_vstream_end(st))
+    return mask, mc

@@ -28,10 +28,18 @@
  *                    Then parent[r] = r.
  *   4. oracle_mcomp: count tuples whose source is reached.
  *   5. oracle_validate: the Graph500 tree-validation invariants V1..V6.
+ *   6. oracle_vstream_*: the same invariants as a streaming pass over the tuples in chunks (the
+ *      caller regenerates the tuple list chunk by chunk from the seed, so full-size graphs need
+ *      not be stored; SURVEY.md §8(c) "it can regenerate them from the seed"), with the tuple
+ *      checks spread over the host cores (OpenMP).  Written separately from oracle_validate,
+ *      which pins it (tests/test_oracle.py).
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef struct {
   uint64_t n;          /* number of vertices */
@@ -84,7 +92,9 @@ void oracle_free(oracle_graph* g) {
 
 uint64_t oracle_num_adjacency(const oracle_graph* g) { return g->off[g->n]; }
 
-/* Number of distinct neighbours of v other than v (degree in G). Used to choose roots. */
+/* Number of adjacency entries of v: non-self-loop tuple endpoints at v, duplicates INCLUDED (so
+ * it is >= the degree of v in G, and > 0 exactly when v has a neighbour other than itself).
+ * Used only as "> 0" for root eligibility (SURVEY.md §8(c) reading 14). */
 uint64_t oracle_degree(const oracle_graph* g, uint64_t v) {
   return g->off[v + 1] - g->off[v];
 }
@@ -207,5 +217,126 @@ int oracle_validate(uint64_t n, uint64_t m, const uint64_t* src, const uint64_t*
   }
   free(found);
   free(uf);
+  return fail;
+}
+
+/* Step 6: streaming validator.  Same bitmask as oracle_validate.
+ *   begin: the per-vertex checks (V1; V5's "unreached have -1/-1, reached have a parent in
+ *          [0,n)"; V3 level[v] == level[parent[v]] + 1);
+ *   feed : one chunk of tuples: V2 marks the tree edges it sees, V4, V6, and the union-find of
+ *          V5 (a concurrent union-find: link the larger root under the smaller one by
+ *          compare-and-swap, so no cycle can form; finds halve paths with plain stores of a
+ *          grand-parent, which stays an ancestor); also counts m_comp (tuples with a reached
+ *          source);
+ *   end  : V2 (every reached v != r had its tree edge among the tuples) and V5 (reached set ==
+ *          the root's component); frees the state and returns the mask.
+ * level / parent are borrowed until end. */
+typedef struct {
+  uint64_t n, root, mcomp;
+  const int32_t* level;
+  const int64_t* parent;
+  unsigned char* found;
+  uint64_t* uf;
+  int fail;
+} oracle_vstream;
+
+oracle_vstream* oracle_vstream_begin(uint64_t n, uint64_t root, const int32_t* level, const int64_t* parent) {
+  oracle_vstream* st = (oracle_vstream*)calloc(1, sizeof(oracle_vstream));
+  if (!st) return NULL;
+  st->n = n;
+  st->root = root;
+  st->level = level;
+  st->parent = parent;
+  if (root >= n) { st->fail = 1; return st; }
+  st->found = (unsigned char*)calloc(n ? n : 1, 1);
+  st->uf = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+  if (!st->found || !st->uf) { free(st->found); free(st->uf); free(st); return NULL; }
+  int fail = 0;
+  if (level[root] != 0 || parent[root] != (int64_t)root) fail |= 1; /* V1 */
+  int64_t v;
+#pragma omp parallel for reduction(| : fail) schedule(static)
+  for (v = 0; v < (int64_t)n; ++v) {
+    st->uf[v] = (uint64_t)v;
+    if (level[v] < 0) {
+      if (level[v] != -1 || parent[v] != -1) fail |= 16; /* V5: unreached are -1 / -1 */
+    } else if (parent[v] < 0 || (uint64_t)parent[v] >= n) {
+      fail |= 16; /* V5: a reached vertex has a parent id */
+    } else if ((uint64_t)v != root) {
+      const int64_t p = parent[v];
+      if (level[p] < 0 || level[v] != level[p] + 1) fail |= 4; /* V3 */
+    }
+  }
+  st->fail = fail;
+  return st;
+}
+
+static uint64_t vs_find(uint64_t* uf, uint64_t x) {
+  for (;;) {
+    uint64_t p = __atomic_load_n(&uf[x], __ATOMIC_RELAXED);
+    if (p == x) return x;
+    uint64_t gp = __atomic_load_n(&uf[p], __ATOMIC_RELAXED);
+    if (gp != p) __atomic_store_n(&uf[x], gp, __ATOMIC_RELAXED); /* path halving */
+    x = gp;
+  }
+}
+
+static void vs_union(uint64_t* uf, uint64_t a, uint64_t b) {
+  for (;;) {
+    uint64_t ra = vs_find(uf, a), rb = vs_find(uf, b);
+    if (ra == rb) return;
+    if (ra < rb) { uint64_t t = ra; ra = rb; rb = t; }
+    uint64_t expect = ra; /* ra is still a root: hang it under the smaller root rb */
+    if (__atomic_compare_exchange_n(&uf[ra], &expect, rb, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) return;
+  }
+}
+
+void oracle_vstream_feed(oracle_vstream* st, uint64_t m, const uint64_t* src, const uint64_t* dst) {
+  if (!st || (st->fail & 16) || st->root >= st->n) return; /* parent[] not usable as an index */
+  const uint64_t n = st->n;
+  const int32_t* level = st->level;
+  const int64_t* parent = st->parent;
+  int fail = 0;
+  uint64_t mc = 0;
+  int64_t k;
+#pragma omp parallel for reduction(| : fail) reduction(+ : mc) schedule(static)
+  for (k = 0; k < (int64_t)m; ++k) {
+    const uint64_t a = src[k], b = dst[k];
+    if (a >= n || b >= n) { fail |= 64; continue; }
+    if (level[a] >= 0) ++mc; /* m_comp: tuple with a reached source, self-loops included */
+    if (a == b) continue;
+    /* V2: the tuple is the tree edge of b (or of a) */
+    if (level[b] > 0 && (uint64_t)parent[b] == a) st->found[b] = 1;
+    if (level[a] > 0 && (uint64_t)parent[a] == b) st->found[a] = 1;
+    /* V4 */
+    if ((level[a] >= 0) != (level[b] >= 0)) fail |= 8;
+    else if (level[a] >= 0 && (level[a] - level[b] > 1 || level[b] - level[a] > 1)) fail |= 8;
+    /* V6, both orientations */
+    if (level[a] >= 0 && level[b] == level[a] + 1 && (uint64_t)parent[b] > a) fail |= 32;
+    if (level[b] >= 0 && level[a] == level[b] + 1 && (uint64_t)parent[a] > b) fail |= 32;
+    vs_union(st->uf, a, b); /* V5 */
+  }
+  st->fail |= fail;
+  st->mcomp += mc;
+}
+
+uint64_t oracle_vstream_mcomp(const oracle_vstream* st) { return st ? st->mcomp : 0; }
+
+int oracle_vstream_end(oracle_vstream* st) {
+  if (!st) return 64;
+  int fail = st->fail;
+  if (!(fail & 16) && st->root < st->n) {
+    const uint64_t n = st->n, root = st->root;
+    const int32_t* level = st->level;
+    const uint64_t rr = vs_find(st->uf, root);
+    int64_t v;
+#pragma omp parallel for reduction(| : fail) schedule(static)
+    for (v = 0; v < (int64_t)n; ++v) {
+      if ((uint64_t)v != root && level[v] > 0 && !st->found[v]) fail |= 2;   /* V2 */
+      if ((vs_find(st->uf, (uint64_t)v) == rr) != (level[v] >= 0)) fail |= 16; /* V5 */
+    }
+  }
+  free(st->found);
+  free(st->uf);
+  free(st);
   return fail;
 }

@@ -33,7 +33,7 @@ class Comm(ctypes.Structure):
 
 class Opts(ctypes.Structure):
     _fields_ = [("edges_per_thread", ctypes.c_int), ("phase_timing", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("exchange", ctypes.c_int), ("peer_exchange", ctypes.c_int)]
+                ("exchange", ctypes.c_int), ("peer_exchange", ctypes.c_int), ("debug_flags", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -58,7 +58,8 @@ class LevelRecord(ctypes.Structure):
 
 
 EXPORTS = ["bfs_nccl_unique_id", "bfs_graph_create", "bfs_graph_info", "bfs_set_opts", "bfs_degree", "bfs_run",
-           "bfs_mcomp", "bfs_level_times", "bfs_destroy", "bfs_strerror", "bfs_last_error"]
+           "bfs_mcomp", "bfs_level_times", "bfs_gather", "bfs_destroy", "bfs_strerror", "bfs_last_error"]
+DEBUG_POS64 = 1
 
 _lib = None
 
@@ -82,6 +83,7 @@ def lib(build: bool = False):
         L.bfs_run.argtypes = [p, u64, p, p, ctypes.POINTER(Stats)]
         L.bfs_mcomp.argtypes = [p, ctypes.POINTER(u64)]
         L.bfs_level_times.argtypes = [p, ctypes.POINTER(LevelRecord), i, ctypes.POINTER(i)]
+        L.bfs_gather.argtypes = [p, p, p, p, p]
         L.bfs_destroy.argtypes = [p]
         L.bfs_destroy.restype = None
         L.bfs_strerror.argtypes = [i]
@@ -133,8 +135,10 @@ XCHG_BITMAP, XCHG_LIST, XCHG_AUTO = 0, 1, 2
 XCHG = {"bitmap": XCHG_BITMAP, "list": XCHG_LIST, "auto": XCHG_AUTO}
 
 
-def make_opts(edges_per_thread=4, phase_timing=False, stream=None, exchange="bitmap", peer_exchange=False) -> Opts:
+def make_opts(edges_per_thread=4, phase_timing=False, stream=None, exchange="bitmap", peer_exchange=False,
+              debug_flags=0) -> Opts:
     o = Opts()
+    o.debug_flags = int(debug_flags)
     o.peer_exchange = 1 if peer_exchange else 0
     o.edges_per_thread = int(edges_per_thread)
     o.phase_timing = 1 if phase_timing else 0
@@ -189,6 +193,10 @@ class Graph:
         level = np.empty(self.info.nout, dtype=np.int32)
         self.run(root, parent, level)
         return level, parent
+
+    def gather(self, parent=None, level=None, parent_all=None, level_all=None):
+        """bfs_gather: this process's outputs -> every rank's outputs on world rank 0 (collective)."""
+        _check(lib().bfs_gather(self._h, _ptr(parent), _ptr(level), _ptr(parent_all), _ptr(level_all)))
 
     def mcomp(self) -> int:
         out = ctypes.c_uint64()

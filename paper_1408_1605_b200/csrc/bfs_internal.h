@@ -52,6 +52,7 @@ struct LevelCtrl {
   uint32_t done;
   uint32_t pad;
   unsigned long long total_new;  // vertices discovered by the last level (all ranks)
+  unsigned long long sum_frontier, sum_edges;  // over all levels (the arrays below stop at kMaxLevels)
   unsigned long long lvl_frontier[kMaxLevels];
   unsigned long long lvl_edges[kMaxLevels];
 };
@@ -60,6 +61,7 @@ struct LevelCtrl {
 struct Geom {
   uint64_t nverts, npad, block;
   int R, C;
+  int nsm = 148;  // SMs of the graph's device (persistent grids are sized by it)
   uint64_t ncols() const { return (uint64_t)R * block; }  // N/C local columns
   uint64_t nrows() const { return (uint64_t)C * block; }  // N/R local rows
   uint64_t words_block() const { return block / 32; }
@@ -142,7 +144,7 @@ struct Graph {
   bool broken = false;
   std::vector<Rank> ranks;  // local ranks (all R*C with loopback)
   std::vector<void*> allocs;  // graph-lifetime device allocations
-  uint64_t hot_h = 0;         // relabeled hot prefix per vertex block (vertices)
+  uint64_t hot_h = 0;         // degree-ordered prefix per vertex block (vertices; the whole block)
   uint32_t* perm_fwd = nullptr;  // [npad] original -> relabeled global id
   LevelInfo* infos = nullptr; // [nlocal] device, one per local rank
   LevelInfo* h_infos = nullptr; // pinned mirror
@@ -171,6 +173,7 @@ struct Graph {
   int ev_levels = 0;
   std::vector<uint64_t> lvl_frontier, lvl_edges;
   uint64_t xbytes = 0, xlists = 0;  // list exchange: bytes sent and list messages in this run
+  uint64_t xlaunches = 0;           // list exchange: kernels launched in this run
   // peer exchange (NEXT-2): NVLink peer mappings of every rank's signal array, set up on first use
   bool peer_ready = false;
   XSig* xsig = nullptr;               // [64] this rank's signal array (slot = sender world rank)

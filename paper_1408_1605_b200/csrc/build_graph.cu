@@ -8,10 +8,10 @@
 // Duplicates collapse and self-loops are dropped.  tdeg[v] counts every input
 // tuple with source v (the m_comp numerator), duplicates and self-loops included.
 //
-// Internal relabeling (layout only): inside every vertex block the H vertices of
-// highest tuple degree are moved to offsets 0..H-1 (degree order), swapping places with the
-// vertices they displace; ownership (the block) never changes and all outputs are in the
-// original ids.  The expansion keeps the visited bits of these hot prefixes in shared memory.
+// Internal relabeling (layout only): inside every vertex block the vertices are
+// renumbered by descending degree; ownership (the block) never changes and all outputs are in the
+// original ids.  The expansion keeps the visited bits of the hot (highest-degree) prefixes in
+// shared memory.
 // To keep the minimum-id parent rule in original ids, CSC rows are ordered by ORIGINAL row id
 // and CSR rows by ORIGINAL column id (the stored indices are the relabeled ones).
 #include <cub/device/device_radix_sort.cuh>
@@ -119,11 +119,6 @@ __global__ void k_degree_keys(const uint32_t* sdeg, uint64_t npad, uint64_t bloc
   }
 }
 
-__global__ void k_iota2(uint32_t* a, uint32_t* b, uint64_t n) {
-  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
-    a[v] = b[v] = (uint32_t)v;
-}
-
 // full per-block degree sort: relabeled id k <- vertex sorted[k] (blocks stay in place: the sort
 // key starts with the block)
 __global__ void k_perm_from_sorted(const uint32_t* sorted, uint64_t n, uint32_t* fwd, uint32_t* inv) {
@@ -131,14 +126,6 @@ __global__ void k_perm_from_sorted(const uint32_t* sorted, uint64_t n, uint32_t*
     const uint32_t v = sorted[k];
     fwd[v] = (uint32_t)k;
     inv[k] = v;
-  }
-}
-
-__global__ void k_apply_moves(const uint32_t* moves, uint64_t nmoves, uint32_t* fwd, uint32_t* inv) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nmoves; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = moves[2 * t], n = moves[2 * t + 1];
-    fwd[o] = n;
-    inv[n] = o;
   }
 }
 
@@ -193,16 +180,15 @@ static int bits_for(uint64_t n) {  // bits to represent values < n
   return b;
 }
 
-// Hot-prefix permutation: perm_fwd (original -> relabeled global id) and perm_inv on device.
+// Degree relabeling: perm_fwd (original -> relabeled global id) and perm_inv on
+// device.  Inside every vertex block the vertices are ordered by descending non-self-loop degree
+// (ties by original id): one radix sort of (block, -degree) keys, then position k of the sorted
+// order is relabeled offset k.
 static int compute_relabel(Graph& G, const uint32_t* sdeg, uint32_t* fwd, uint32_t* inv) {
   cudaStream_t s = G.stream;
   const Geom& g = G.g;
   const uint64_t P = (uint64_t)g.R * g.C;
-  const uint64_t H = G.hot_h;
   Scratch sc;
-  k_iota2<<<4096, 256, 0, s>>>(fwd, inv, g.npad);
-  CKR(cudaGetLastError());
-  if (H == 0) return BFS_OK;
   ull *keys = nullptr, *keys2 = nullptr;
   uint32_t *vals = nullptr, *vals2 = nullptr;
   void* tmp = nullptr;
@@ -217,47 +203,8 @@ static int compute_relabel(Graph& G, const uint32_t* sdeg, uint32_t* fwd, uint32
   k_degree_keys<<<4096, 256, 0, s>>>(sdeg, g.npad, g.block, keys, vals);
   CKR(cudaGetLastError());
   CKR(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (uint64_t)g.npad, 0, kb, s));
-  if (H >= g.block) {  // the whole block in degree order: position k holds vertex vals2[k]
-    k_perm_from_sorted<<<4096, 256, 0, s>>>(vals2, g.npad, fwd, inv);
-    CKR(cudaGetLastError());
-    CKR(cudaStreamSynchronize(s));
-    return BFS_OK;
-  }
-  std::vector<uint32_t> hot(P * H);
-  for (uint64_t b = 0; b < P; ++b)
-    CKR(cudaMemcpyAsync(hot.data() + b * H, vals2 + b * g.block, H * 4, cudaMemcpyDeviceToHost, s));
-  CKR(cudaStreamSynchronize(s));
-  // moves: hot vertex t_q -> offset q; displaced occupant of a low offset q -> a vacated offset
-  std::vector<uint32_t> moves;
-  moves.reserve(P * H * 4);
-  std::vector<char> low_hot(H);
-  for (uint64_t b = 0; b < P; ++b) {
-    const uint64_t vb = b * g.block;
-    std::fill(low_hot.begin(), low_hot.end(), 0);
-    std::vector<uint64_t> vacated;
-    for (uint64_t q = 0; q < H; ++q) {
-      const uint64_t t = hot[b * H + q] - vb;
-      if (t < H) low_hot[t] = 1; else vacated.push_back(t);
-      if (t != q) {
-        moves.push_back((uint32_t)(vb + t));
-        moves.push_back((uint32_t)(vb + q));
-      }
-    }
-    size_t k = 0;
-    for (uint64_t q = 0; q < H; ++q)
-      if (!low_hot[q]) {
-        moves.push_back((uint32_t)(vb + q));
-        moves.push_back((uint32_t)(vb + vacated[k++]));
-      }
-  }
-  const uint64_t nm = moves.size() / 2;
-  if (nm) {
-    uint32_t* dm = nullptr;
-    CKR(sc.alloc(&dm, moves.size() * 4));
-    CKR(cudaMemcpyAsync(dm, moves.data(), moves.size() * 4, cudaMemcpyHostToDevice, s));
-    k_apply_moves<<<1024, 256, 0, s>>>(dm, nm, fwd, inv);
-    CKR(cudaGetLastError());
-  }
+  k_perm_from_sorted<<<4096, 256, 0, s>>>(vals2, g.npad, fwd, inv);
+  CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
   return BFS_OK;
 }
@@ -353,14 +300,15 @@ static int rank_maps(Graph& G, Rank& rk, const uint32_t* fwd, const uint32_t* in
   if ((rc = G_alloc(G, (void**)&rk.inv_own, g.block * 4))) return rc;
   if ((rc = G_alloc(G, (void**)&rk.inv_col, g.ncols() * 4))) return rc;
   {
+    Scratch sc;
     ull* cnt = nullptr;
     ull h = 0;
-    CKR(cudaMalloc(&cnt, sizeof(ull)));
+    CKR(sc.alloc(&cnt, sizeof(ull)));
     CKR(cudaMemsetAsync(cnt, 0, sizeof(ull), s));
     k_count_nz_rows<<<1024, 256, 0, s>>>(rk.csr_ptr, g.nrows(), cnt);
+    CKR(cudaGetLastError());
     CKR(cudaMemcpyAsync(&h, cnt, sizeof(ull), cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
-    cudaFree(cnt);
     rk.nz_rows = h;
   }
   const uint64_t vb = (uint64_t)rk.r * g.block;

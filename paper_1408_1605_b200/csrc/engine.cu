@@ -28,6 +28,9 @@ namespace bfs200 {
 
 typedef unsigned long long ull;
 
+// head of LevelCtrl read by the host each level (everything before the per-level arrays)
+constexpr size_t kCtrlHead = offsetof(LevelCtrl, lvl_frontier);
+
 static thread_local std::string tl_err;
 
 int set_err(int status, const char* fmt, ...) {
@@ -258,6 +261,7 @@ static int check_opts(const bfs_opts* o) {
     return set_err(BFS_EINVAL, "exchange must be 0 (bitmap), 1 (list) or 2 (auto) (got %d)", o->exchange);
   if (o->peer_exchange != 0 && o->peer_exchange != 1)
     return set_err(BFS_EINVAL, "peer_exchange must be 0 or 1 (got %d)", o->peer_exchange);
+  if (o->debug_flags & ~BFS_DEBUG_POS64) return set_err(BFS_EINVAL, "unknown debug_flags 0x%x", o->debug_flags);
   if (o->peer_exchange && o->exchange != BFS_XCHG_BITMAP)
     return set_err(BFS_EINVAL, "peer_exchange needs exchange = 0 (bitmap messages)");
   return BFS_OK;
@@ -304,14 +308,14 @@ static int create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, uin
   G.g.R = R;
   G.g.C = C;
   G.g.block = G.g.npad / P;
-  {  // degree-ordered prefix per vertex block: by default the whole block (a full
-     // degree sort); BFS200_HOT_PREFIX sets a shorter prefix (experiments)
-    const char* env = getenv("BFS200_HOT_PREFIX");
-    const uint64_t want = (env && atoll(env) > 0) ? (uint64_t)atoll(env) : ~0ull;
-    G.hot_h = G.g.block < want ? G.g.block : want;
-    G.hot_h &= ~31ull;
-    if (!G.hot_h) G.hot_h = G.g.block;
+  // degree-ordered relabeling of every whole vertex block
+  G.hot_h = G.g.block;
+  {
+    int nsm = 0;
+    CKR(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, G.device));
+    G.g.nsm = nsm > 0 ? nsm : 148;
   }
+  CKR(kernels_init_device());
   G.ntuples = nedges;
   CKR(cudaMallocHost(&G.h_scratch, 16 * sizeof(ull)));
   {
@@ -363,7 +367,7 @@ static int ev_prepare(Graph& G, int level) {
 }
 
 static inline int ev_rec(Graph& G, int level, int p) {
-  if (!G.opts.phase_timing) return BFS_OK;
+  if (!G.opts.phase_timing || level >= kMaxLevels) return BFS_OK;  // per-level records stop at kMaxLevels
   int rc = ev_prepare(G, level);
   if (rc) return rc;
   CKR(cudaEventRecord(G.ev[(size_t)level * kPhaseEvents + p], G.stream));
@@ -386,52 +390,67 @@ static int setup_peer(Graph& G) {
   cudaStream_t s = G.stream;
   Rank& rk = G.ranks[0];
   int rc;
+  // Every step up to the agreement below is collective-safe: a local failure is recorded (not
+  // returned), the rank still takes part in the handle all-gather, and the failure flag is then
+  // all-reduced, so every rank returns the same error instead of some ranks waiting forever in
+  // a collective that a failed rank never joins.
+  int local_fail = 0;
+  std::string why;
+  auto fail = [&](const char* what, cudaError_t e) {
+    if (!local_fail) why = std::string(what) + ": " + cudaGetErrorString(e);
+    local_fail = 1;
+    cudaGetLastError();
+  };
   if ((rc = G_alloc(G, (void**)&G.xsig, 64 * sizeof(XSig)))) return rc;
-  CKR(cudaMemset(G.xsig, 0, 64 * sizeof(XSig)));
   if ((rc = G_alloc(G, (void**)&G.d_epoch, 8))) return rc;
-  CKR(cudaMemset(G.d_epoch, 0, 8));
   if ((rc = G_alloc(G, (void**)&G.d_xerr, 8))) return rc;
-  CKR(cudaMemset(G.d_xerr, 0, 8));
   // C == 1: no fold / resolution buffers; dummies keep the handle layout uniform
   if (!rk.recv && (rc = G_alloc(G, (void**)&rk.recv, 16))) return rc;
   if (!rk.reqin && (rc = G_alloc(G, (void**)&rk.reqin, 16))) return rc;
   if (!rk.respin && (rc = G_alloc(G, (void**)&rk.respin, 16))) return rc;
+  CKR(cudaMemset(G.xsig, 0, 64 * sizeof(XSig)));
+  CKR(cudaMemset(G.d_epoch, 0, 8));
+  CKR(cudaMemset(G.d_xerr, 0, 8));
   constexpr int NH = 5;
   cudaIpcMemHandle_t mine[NH];
-  CKR(cudaIpcGetMemHandle(&mine[0], rk.recv));
-  CKR(cudaIpcGetMemHandle(&mine[1], rk.all_front));
-  CKR(cudaIpcGetMemHandle(&mine[2], G.xsig));
-  CKR(cudaIpcGetMemHandle(&mine[3], rk.reqin));
-  CKR(cudaIpcGetMemHandle(&mine[4], rk.respin));
+  memset(mine, 0, sizeof mine);
+  void* const bufs[NH] = {rk.recv, rk.all_front, G.xsig, rk.reqin, rk.respin};
+  for (int k = 0; k < NH && !local_fail; ++k) {
+    const cudaError_t e = cudaIpcGetMemHandle(&mine[k], bufs[k]);
+    if (e != cudaSuccess) fail("peer_exchange: cudaIpcGetMemHandle", e);
+  }
   const size_t hb = sizeof(mine);
+  Scratch sc;
   unsigned char* dbuf = nullptr;
-  CKR(cudaMalloc(&dbuf, hb * (P + 1)));
+  CKR(sc.alloc(&dbuf, hb * (P + 1)));
   CKR(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice));
   NKR(ncclAllGather(dbuf, dbuf + hb, hb, ncclUint8, G.world, s));
   std::vector<cudaIpcMemHandle_t> all((size_t)P * NH);
   CKR(cudaMemcpyAsync(all.data(), dbuf + hb, hb * P, cudaMemcpyDeviceToHost, s));
   CKR(cudaStreamSynchronize(s));
-  cudaFree(dbuf);
-  std::vector<std::vector<void*>> of(NH, std::vector<void*>(P));  // [buffer][rank]
-  for (int p = 0; p < P; ++p) {
-    if (p == me) {
-      of[0][p] = rk.recv;
-      of[1][p] = rk.all_front;
-      of[2][p] = G.xsig;
-      of[3][p] = rk.reqin;
-      of[4][p] = rk.respin;
-      continue;
-    }
-    for (int k = 0; k < NH; ++k) {
+  std::vector<std::vector<void*>> of(NH, std::vector<void*>(P, nullptr));  // [buffer][rank]
+  for (int p = 0; p < P && !local_fail; ++p) {
+    for (int k = 0; k < NH && !local_fail; ++k) {
+      if (p == me) {
+        of[k][p] = bufs[k];
+        continue;
+      }
       void* ptr = nullptr;
-      cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)p * NH + k], cudaIpcMemLazyEnablePeerAccess);
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)p * NH + k], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
-        cudaGetLastError();
-        return set_err(BFS_ECUDA, "peer_exchange: cudaIpcOpenMemHandle of rank %d failed: %s", p,
-                       cudaGetErrorString(e));
+        fail("peer_exchange: cudaIpcOpenMemHandle (no CUDA IPC / peer access between the ranks' GPUs?)", e);
+        break;
       }
       G.ipc_opened.push_back(ptr);
       of[k][p] = ptr;
+    }
+  }
+  {  // agreement: any rank's failure fails every rank (the graph is then unusable everywhere)
+    int any = local_fail;
+    if ((rc = comm_allreduce_int_max(G, &any))) return rc;
+    if (any) {
+      G.broken = true;
+      return set_err(BFS_ECUDA, "%s", local_fail ? why.c_str() : "peer_exchange: setup failed on another rank");
     }
   }
   const std::vector<void*>&recv_of = of[0], &front_of = of[1], &sig_of = of[2], &reqin_of = of[3],
@@ -503,7 +522,7 @@ static int expand_exchange_x(Graph& G) {
   std::vector<ull> cnt((size_t)G.ranks.size() * 64, 0);
   for (Rank& rk : G.ranks) {
     CKR(cudaMemsetAsync(rk.xcnt, 0, 64 * 8, s));
-    CKR(launch_seg_popc(rk.all_front + (uint64_t)rk.i * W, W, 1, rk.xcnt, s));
+    CKR(launch_seg_popc(rk.all_front + (uint64_t)rk.i * W, W, 1, rk.xcnt, &G.xlaunches, s));
   }
   if (G.world_size > 1) {
     Rank& rk = G.ranks[0];
@@ -541,14 +560,14 @@ static int expand_exchange_x(Graph& G) {
     G.xlists += (ull)(g.R - 1);
     if (G.world_size > 1) {
       CKR(launch_list_encode(dst.all_front + (uint64_t)dst.i * W, W, 1, dst.xoff, dst.xtmp, dst.xtmp_bytes, dst.xsend,
-                             g.block, s));
+                             g.block, g.nsm, &G.xlaunches, s));
       if (maxn) NKR(ncclAllGather(dst.xsend, dst.xrecv, maxn, ncclUint32, G.colc, s));
     } else {
       for (int i2 = 0; i2 < g.R; ++i2) {
         if (i2 == dst.i) continue;
         Rank& src = G.ranks[dst.j * g.R + i2];
         CKR(launch_list_encode(src.all_front + (uint64_t)i2 * W, W, 1, src.xoff, src.xtmp, src.xtmp_bytes, src.xsend,
-                               g.block, s));
+                               g.block, g.nsm, &G.xlaunches, s));
         const ull n = n_of(dst, i2);
         if (n) CKR(cudaMemcpyAsync(dst.xrecv + i2 * maxn, src.xsend, n * 4, cudaMemcpyDeviceToDevice, s));
       }
@@ -558,7 +577,7 @@ static int expand_exchange_x(Graph& G) {
       const ull n = n_of(dst, i2);
       G.xbytes += n * 4;
       CKR(cudaMemsetAsync(dst.all_front + i2 * W, 0, W * 4, s));
-      CKR(launch_list_scatter(dst.xrecv + i2 * maxn, n, dst.all_front + i2 * W, s));
+      CKR(launch_list_scatter(dst.xrecv + i2 * maxn, n, dst.all_front + i2 * W, g.nsm, &G.xlaunches, s));
     }
   }
   return BFS_OK;
@@ -576,7 +595,7 @@ static int fold_exchange_x(Graph& G) {
   std::vector<ull> cnt(nl * 64, 0), rcnt(64, 0);
   for (Rank& rk : G.ranks) {
     CKR(cudaMemsetAsync(rk.xcnt, 0, 64 * 8, s));
-    CKR(launch_seg_popc(rk.sendbuf, W, g.C, rk.xcnt, s));
+    CKR(launch_seg_popc(rk.sendbuf, W, g.C, rk.xcnt, &G.xlaunches, s));
   }
   if (G.world_size > 1) {
     Rank& rk = G.ranks[0];
@@ -600,7 +619,7 @@ static int fold_exchange_x(Graph& G) {
   }
   // encode every outgoing segment as a list (segments sent as bitmaps ignore theirs)
   for (Rank& rk : G.ranks)
-    CKR(launch_list_encode(rk.sendbuf, W, g.C, rk.xoff, rk.xtmp, rk.xtmp_bytes, rk.xsend, g.block, s));
+    CKR(launch_list_encode(rk.sendbuf, W, g.C, rk.xoff, rk.xtmp, rk.xtmp_bytes, rk.xsend, g.block, g.nsm, &G.xlaunches, s));
   if (G.world_size > 1) {
     Rank& rk = G.ranks[0];
     NKR(ncclGroupStart());
@@ -625,7 +644,7 @@ static int fold_exchange_x(Graph& G) {
     for (int c = 0; c < g.C; ++c) {
       if (c == rk.j || !use_list(G, rcnt[c])) continue;
       CKR(cudaMemsetAsync(rk.recv + (uint64_t)c * W, 0, W * 4, s));
-      CKR(launch_list_scatter(rk.xrecv + (uint64_t)c * g.block, rcnt[c], rk.recv + (uint64_t)c * W, s));
+      CKR(launch_list_scatter(rk.xrecv + (uint64_t)c * g.block, rcnt[c], rk.recv + (uint64_t)c * W, g.nsm, &G.xlaunches, s));
     }
   } else {
     for (size_t kd = 0; kd < nl; ++kd) {
@@ -642,7 +661,7 @@ static int fold_exchange_x(Graph& G) {
             CKR(cudaMemcpyAsync(dst.xrecv + (uint64_t)c * g.block, src.xsend + (uint64_t)dst.j * g.block, n * 4,
                                 cudaMemcpyDeviceToDevice, s));
           CKR(cudaMemsetAsync(dst.recv + (uint64_t)c * W, 0, W * 4, s));
-          CKR(launch_list_scatter(dst.xrecv + (uint64_t)c * g.block, n, dst.recv + (uint64_t)c * W, s));
+          CKR(launch_list_scatter(dst.xrecv + (uint64_t)c * g.block, n, dst.recv + (uint64_t)c * W, g.nsm, &G.xlaunches, s));
         } else {
           G.xbytes += W * 4;
           CKR(cudaMemcpyAsync(dst.recv + (uint64_t)c * W, src.sendbuf + (uint64_t)dst.j * W, W * 4,
@@ -751,7 +770,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
     if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
     CKR(launch_scan(g, rk, tile_edges, s));
     if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
-    CKR(launch_expand(g, rk, E, G.hot_h, s));
+    CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
     if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
     CKR(launch_parent(g, rk, s));
     if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
@@ -772,7 +791,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
   if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, s));
+  for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
   if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
   if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
@@ -827,7 +846,14 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   const uint64_t owner = root / g.block;
   bool owner_local = false;
   int rcp;
-  if (peer_active(G) && (rcp = setup_peer(G))) return rcp;
+  if (peer_active(G)) {
+    if ((rcp = setup_peer(G))) return rcp;
+    // Rendezvous on the stream before the first cross-GPU flag barrier: NCCL waits for a late
+    // rank without a timeout, so a caller that reaches bfs_run long after its peers (e.g. after
+    // validating the previous result on the host) is not mistaken for a dead peer by the bounded
+    // spin of k_xbarrier.  The max also spreads any earlier barrier error to every rank.
+    NKR(ncclAllReduce(G.d_xerr, G.d_xerr, 1, ncclInt, ncclMax, G.world, s));
+  }
   for (Rank& rk : G.ranks) {
     owner_local |= (uint64_t)rk.r == owner;
     CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, s));
@@ -841,28 +867,30 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   // graph mode: no phase events, and not on the very first run (which initialises the kernels'
   // launch attributes outside of any capture)
   bool use_graph = !G.opts.phase_timing && !G.graph_failed && G.runs > 0 && G.opts.exchange == BFS_XCHG_BITMAP;
-  G.xbytes = G.xlists = 0;
-  const uint64_t xk0 = list_kernel_launches();
+  G.xbytes = G.xlists = G.xlaunches = 0;
   if (G.opts.exchange != BFS_XCHG_BITMAP && (rc = alloc_xchg(G))) return rc;
   if (use_graph && (!G.gexec || G.graph_stream != s || G.graph_E != G.opts.edges_per_thread ||
                     G.graph_peer != peer_active(G))) {
     if (build_level_graph(G) != BFS_OK) {
-      // orchestration fallback only (same kernels, host-driven loop); clear the sticky state
+      // Capture or instantiation of the level graph failed (e.g. a driver without conditional
+      // nodes): fall back to the host-driven loop, which runs the same kernels.  Only errors of
+      // the capture itself are forgiven: the (non-sticky) error is cleared, and the device must
+      // then still synchronise cleanly -- a sticky error leaves the graph broken.
       G.graph_failed = true;
-      G.broken = false;
-      cudaGetLastError();
       drop_graph(G);
       use_graph = false;
-      cudaStreamSynchronize(s);
+      cudaGetLastError();
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_fail(G, e, "device unhealthy after a failed level-graph capture", __FILE__, __LINE__);
+      G.broken = false;
     }
   }
   if (use_graph) {
     CKR(cudaGraphLaunch(G.gexec, s));
   } else {
     for (int nlev = 0;; ++nlev) {
-      if (nlev >= kMaxLevels) return set_err(BFS_ESTATE, "level limit exceeded");
       if ((rc = enqueue_level(G, false, nlev))) return rc;
-      CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
+      CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, kCtrlHead, cudaMemcpyDeviceToHost, s));
       CKR(cudaStreamSynchronize(s));
       if (G.h_ctrl->done) break;
     }
@@ -918,25 +946,24 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
   }
   // per-level statistics of the device-side loop
-  CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, 32, cudaMemcpyDeviceToHost, s));
+  CKR(cudaMemcpyAsync(G.h_ctrl, G.d_ctrl, kCtrlHead, cudaMemcpyDeviceToHost, s));
   CKR(cudaStreamSynchronize(s));
   const int nlev = (int)G.h_ctrl->nlev;
-  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_frontier, G.d_ctrl->lvl_frontier, nlev * sizeof(ull), cudaMemcpyDeviceToHost, s));
-  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_edges, G.d_ctrl->lvl_edges, nlev * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  const int nrec = nlev < kMaxLevels ? nlev : kMaxLevels;  // per-level records kept
+  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_frontier, G.d_ctrl->lvl_frontier, nrec * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  CKR(cudaMemcpyAsync(G.h_ctrl->lvl_edges, G.d_ctrl->lvl_edges, nrec * sizeof(ull), cudaMemcpyDeviceToHost, s));
   CKR(cudaStreamSynchronize(s));
   G.last_levels = nlev;
-  G.lvl_frontier.assign(G.h_ctrl->lvl_frontier, G.h_ctrl->lvl_frontier + nlev);
-  G.lvl_edges.assign(G.h_ctrl->lvl_edges, G.h_ctrl->lvl_edges + nlev);
+  G.lvl_frontier.assign(G.h_ctrl->lvl_frontier, G.h_ctrl->lvl_frontier + nrec);
+  G.lvl_edges.assign(G.h_ctrl->lvl_edges, G.h_ctrl->lvl_edges + nrec);
   const ull bytes = (ull)nlev * G.ranks.size() * ((ull)(g.R - 1) + (ull)(g.C - 1)) * W * 4;
   G.has_run = true;
   ++G.runs;
   if (stats) {
     memset(stats, 0, sizeof *stats);
     stats->nlevels = nlev;
-    for (int l = 0; l < nlev; ++l) {
-      stats->edges_scanned += G.lvl_edges[l];
-      stats->frontier_columns += G.lvl_frontier[l];
-    }
+    stats->edges_scanned = G.h_ctrl->sum_edges;
+    stats->frontier_columns = G.h_ctrl->sum_frontier;
     stats->bytes_exchanged = G.opts.exchange == BFS_XCHG_BITMAP ? bytes : G.xbytes;
     stats->list_messages = G.xlists;
     if (G.opts.phase_timing) {  // the stream is synchronised: reading the events costs nothing
@@ -955,7 +982,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     const int owner_j = (int)(owner / (uint64_t)g.R);
     stats->kernel_launches =
         (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
-        (list_kernel_launches() - xk0) +
+        G.xlaunches +
         (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
   }
   return BFS_OK;
@@ -1100,13 +1127,72 @@ int bfs_mcomp(bfs_graph* gp, uint64_t* m_comp) {
   return BFS_OK;
 }
 
+int bfs_gather(bfs_graph* gp, const int64_t* parent, const int32_t* level, int64_t* parent_all, int32_t* level_all) {
+  ENTER(gp);
+  const Geom& g = G.g;
+  const uint64_t nout = (uint64_t)G.ranks.size() * g.block;  // this process's slice
+  const bool root = G.world_rank == 0;
+  cudaStream_t s = G.stream;
+  if (root && ((parent && !parent_all) || (level && !level_all)))
+    return set_err(BFS_EINVAL, "rank 0 needs parent_all / level_all for every non-NULL input");
+  try {
+    if (G.world_size == 1) {  // one process holds every rank: the slice is the whole vertex range
+      if (parent) CKR(cudaMemcpyAsync(parent_all, parent, nout * 8, cudaMemcpyDefault, s));
+      if (level) CKR(cudaMemcpyAsync(level_all, level, nout * 4, cudaMemcpyDefault, s));
+      CKR(cudaStreamSynchronize(s));
+      return BFS_OK;
+    }
+    // one process per rank: rank r's slice is global [r*block, (r+1)*block); point-to-point sends
+    // to rank 0 over the world communicator (device staging where the caller's buffers are host)
+    const int P = G.world_size;
+    auto gather_one = [&](const void* mine, void* all, size_t esz, ncclDataType_t dt) -> int {
+      Scratch sc;
+      const void* src = mine;
+      if (!is_device_ptr(mine)) {
+        void* st = nullptr;
+        CKR(sc.alloc(&st, nout * esz));
+        CKR(cudaMemcpyAsync(st, mine, nout * esz, cudaMemcpyHostToDevice, s));
+        src = st;
+      }
+      void* dst = nullptr;
+      if (root) {
+        if (is_device_ptr(all)) {
+          dst = all;
+        } else {
+          CKR(sc.alloc(&dst, (size_t)P * nout * esz));
+        }
+      }
+      NKR(ncclGroupStart());
+      if (root) {
+        for (int q = 1; q < P; ++q)
+          NKR(ncclRecv(static_cast<char*>(dst) + (size_t)q * nout * esz, nout, dt, q, G.world, s));
+      } else {
+        NKR(ncclSend(src, nout, dt, 0, G.world, s));
+      }
+      NKR(ncclGroupEnd());
+      if (root) {
+        CKR(cudaMemcpyAsync(dst, src, nout * esz, cudaMemcpyDeviceToDevice, s));
+        if (dst != all) CKR(cudaMemcpyAsync(all, dst, (size_t)P * nout * esz, cudaMemcpyDeviceToHost, s));
+      }
+      CKR(cudaStreamSynchronize(s));
+      return BFS_OK;
+    };
+    int rc;
+    if (parent && (rc = gather_one(parent, parent_all, 8, ncclInt64))) return rc;
+    if (level && (rc = gather_one(level, level_all, 4, ncclInt32))) return rc;
+    return BFS_OK;
+  } catch (std::bad_alloc&) {
+    return set_err(BFS_ENOMEM, "host allocation failed");
+  }
+}
+
 int bfs_level_times(bfs_graph* gp, bfs_level_record* out, int max_levels, int* nlevels) {
   ENTER(gp);
   if (!nlevels) return set_err(BFS_EINVAL, "null nlevels");
   if (!G.has_run) return set_err(BFS_ESTATE, "no BFS has run on this graph");
   if (!G.opts.phase_timing) return set_err(BFS_ESTATE, "phase_timing was off for the last run");
-  *nlevels = G.last_levels;
-  const int n = G.last_levels < max_levels ? G.last_levels : max_levels;
+  *nlevels = G.last_levels < kMaxLevels ? G.last_levels : kMaxLevels;  // records kept (first kMaxLevels levels)
+  const int n = *nlevels < max_levels ? *nlevels : max_levels;
   if (n > 0 && !out) return set_err(BFS_EINVAL, "null output");
   for (int l = 0; l < n; ++l) {
     float t[kPhaseEvents - 1];

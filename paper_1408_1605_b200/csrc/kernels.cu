@@ -72,58 +72,10 @@ __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
                ::"l"(a), "r"(m), "r"((int)p));
 }
 
-// mbarrier + 1D bulk copy (TMA engine, UBLKCP): global -> shared without registers or L1
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_inval(uint32_t bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
-#ifndef BFS200_RING_EF
-#define BFS200_RING_EF 0
-#endif
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-#if BFS200_RING_EF
-  // streamed once: evict-first in L2, so the visited/discovered lines stay resident
-  asm volatile(
-      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-#else
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-#endif
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      " WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT;\n"
-      "}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
-}
-
-static int g_num_sms = 0;
-static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
 }
 
 // ------------------------------------------------------------------ init (Alg.2 lines 1-10)
@@ -142,9 +94,10 @@ __global__ void k_seed_root(uint32_t* vd, uint32_t* all_front, int32_t* level, u
 // reader masks with the visited bit (unreached -> -1).
 cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s) {
   const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
-  cudaMemsetAsync(rk.vd, 0, 2 * rw * 4, s);
-  cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
-  cudaMemsetAsync(&rk.info->disc_total, 0, sizeof(ull), s);
+  cudaError_t e = cudaMemsetAsync(rk.vd, 0, 2 * rw * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(&rk.info->disc_total, 0, sizeof(ull), s);
+  if (e != cudaSuccess) return e;
   if (owner) {
     const uint64_t t = root - (uint64_t)rk.r * g.block;
     k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
@@ -275,6 +228,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
 #define BFS200_BLIND3 1
 #endif
 constexpr bool kBlind3 = BFS200_BLIND3;
+
+// Parent-claim mode thresholds (k_level_info; measured at s26): P2 when a row's
+// expected CSR scan is <= kP2Factor entries; mode 3 when the P1 candidate edges are >= rows / kM3Factor.
+constexpr ull kP2Factor = 8;
+constexpr ull kM3Factor = 4;
 
 // level totals from the segment scan (seg_off[nseg] = sum over all segments); resets counters
 __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* info, ull* cumul, ull nnz,
@@ -526,21 +484,11 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   // exclusive scan over nseg+1 segment totals (st[nseg] stays zero) -> so[nseg] = level total
   cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0u, 0u, 0ull, 0ull},
                                  (uint64_t)nseg + 1, s);
-  static ull p2_factor = 0;
-  if (!p2_factor) {  // tuning knob for experiments: BFS200_P2_FACTOR (default 8)
-    const char* env = getenv("BFS200_P2_FACTOR");
-    p2_factor = (env && atoi(env) > 0) ? (ull)atoi(env) : 8ull;
-  }
-  static long m3_factor = -1;
-  if (m3_factor < 0) {  // tuning knob for experiments: BFS200_M3_FACTOR (0 disables mode 3; default 4)
-    const char* env = getenv("BFS200_M3_FACTOR");
-    m3_factor = env ? atol(env) : 4;
-  }
-  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, p2_factor, (ull)rk.nz_rows,
-                               (ull)m3_factor, (ull)g.nrows());
+  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows, kM3Factor,
+                               (ull)g.nrows());
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
-  k_tile_fill<<<num_sms() * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
+  k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
   return cudaGetLastError();
 }
 
@@ -559,30 +507,10 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
 constexpr size_t kSmemTarget = 160 * 1024;  // K1 dynamic shared memory (staging + hot copy)
-// Long-column tiles of a P2 level in flight per warp: their `row` entries are fetched by 1D bulk
-// copies (cp.async.bulk, TMA engine) into a per-warp shared-memory ring, so the bytes in flight
-// are bounded by the ring, not by registers or L1 capacity.  0 = register loads (double-buffered).
-#ifndef BFS200_RING
-#define BFS200_RING 0
-#endif
-constexpr int kRing = BFS200_RING;
-#ifndef BFS200_DEFER
-#define BFS200_DEFER 0
-#endif
-constexpr bool kDefer = BFS200_DEFER;  // ring loop: a tile's REDs after the next tile's probes
-// per-warp ring: kRing mbarriers (padded to 16 B), then kRing slots of TILE + 4 words (a tile's
-// range rounded out to 16-B boundaries: up to 3 leading words)
-template <int E>
-__host__ __device__ constexpr size_t ring_bytes_per_warp() {
-  return kRing ? 16 * ((kRing * 8 + 15) / 16) + (size_t)kRing * (32 * E + 4) * 4 : 0;
-}
-// per-warp chunk before the hot-copy region: the warp's short-tile staging (s_off, s_beg) and its
-// long-tile ring overlay each other (a warp finishes its long tiles before it stages short ones)
+// per-warp chunk before the hot-copy region: the warp's short-tile staging (s_off, s_beg)
 template <int E>
 __host__ __device__ constexpr size_t expand_warp_bytes(bool pos32) {
-  return 16 * (((32 * E + 2) * ((pos32 ? 4 : 8) + 4) > ring_bytes_per_warp<E>()
-                    ? ((32 * E + 2) * ((pos32 ? 4 : 8) + 4) + 15) / 16
-                    : (ring_bytes_per_warp<E>() + 15) / 16));
+  return 16 * (((32 * E + 2) * ((pos32 ? 4 : 8) + 4) + 15) / 16);
 }
 template <int E, int THREADS>
 __host__ __device__ constexpr size_t expand_stage_bytes(bool pos32) {
@@ -670,23 +598,6 @@ __device__ __forceinline__ void probe_red(const Probe& p) {
                " setp.eq.and.b32 pr, t, 0, pn;\n"
                " @pr red.relaxed.gpu.global.or.b32 [%4+4], %2;\n"
                "}" ::"r"(p.x), "r"(p.y), "r"(p.m), "r"(p.need), "l"(p.a));
-}
-
-// Deferred form of probe_red for a row v whose probe result (x, y, need) was kept in registers
-// (the ring loop issues the next tile's probes before this RED; the bit is idempotent).
-__device__ __forceinline__ void red_deferred(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
-  asm volatile("{\n"
-               " .reg .pred pn, pr;\n"
-               " .reg .b32 t, m;\n"
-               " .reg .b64 a;\n"
-               " setp.ne.b32 pn, %3, 0;\n"
-               " shf.l.wrap.b32 m, 0, 1, %0;\n"
-               " lop3.b32 t, %1, %2, m, 0xa8;\n"
-               " setp.eq.and.b32 pr, t, 0, pn;\n"
-               " shr.b32 t, %0, 5;\n"
-               " mad.wide.u32 a, t, 8, %4;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
-               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
 }
 
 // One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
@@ -813,91 +724,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       }
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
-    if constexpr (!P1 && kRing > 0) {
-      // ring of kRing bulk-copied tiles per warp; slot s holds tiles t + (kRing*k + s)*stride
-      constexpr uint32_t SW = TILE + 4;  // slot words
-      constexpr uint32_t BARB = 16 * ((kRing * 8 + 15) / 16);
-      unsigned char* wring = wchunk;
-      const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(wring);
-      const uint32_t slot0 = bar0 + BARB;
-      const uint32_t* slots = reinterpret_cast<const uint32_t*>(wring + BARB);
-      if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < kRing; ++s) mbar_init(bar0 + 8 * s, 1);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // inits visible to the copy engine
-      }
-      __syncwarp();
-      uint32_t ro[kRing], rl[kRing];  // per slot: leading words, tile length
-      ull ti = t;                     // next tile to issue, its record already loaded
-      uint4 nrec = ti < nA ? tileA[ti] : make_uint4(0, 0, 0, 0);
-      auto issue = [&](const int s) {
-        const ull pos = (ull)nrec.x | ((ull)nrec.y << 32);
-        const uint32_t o = (uint32_t)pos & 3u;
-        ro[s] = o;
-        rl[s] = nrec.z;
-        if (lane == 0)
-          bulk_g2s(slot0 + s * SW * 4, row + (pos - o), ((o + nrec.z) * 4u + 15u) & ~15u, bar0 + 8 * s);
-        ti += stride;
-        nrec = ti < nA ? tileA[ti] : make_uint4(0, 0, 0, 0);
-      };
-#pragma unroll
-      for (int s = 0; s < kRing; ++s)
-        if (ti < nA) issue(s);
-      uint32_t parity = 0;
-      uint32_t pv[E], px[E], py[E], pn[E];  // kDefer: the previous tile's rows and probe results
-      bool have = false;
-      while (t < nA) {
-#pragma unroll
-        for (int s = 0; s < kRing; ++s) {
-          if (t + (ull)s * stride < nA) {  // warp-uniform
-            mbar_wait(bar0 + 8 * s, parity);
-            uint32_t v[E];
-            const uint32_t* sp = slots + s * SW + ro[s] + lane;
-#pragma unroll
-            for (int q = 0; q < E; ++q) v[q] = sp[32 * q];  // Alg.3 line 4 (lanes past len: unused)
-            const uint32_t len = rl[s];
-            __syncwarp();  // every lane has read the slot: refill it
-            if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (ti < nA) issue(s);
-            Probe pr[E];
-#pragma unroll
-            for (int q = 0; q < E; ++q) {  // Alg.3 lines 5-6
-              if (SEG1) probe_seg1(pr[q], v[q], 32u * q + lane, len, hw, sa, vd);
-              else probe_segs(pr[q], v[q], 32u * q + lane, len, hw, sa, vd, bl, bmask);
-            }
-            if (kDefer) {  // the previous tile's REDs while this tile's probes are in flight
-              if (have) {
-#pragma unroll
-                for (int q = 0; q < E; ++q) red_deferred(pv[q], px[q], py[q], pn[q], vd);
-              }
-#pragma unroll
-              for (int q = 0; q < E; ++q) {
-                pv[q] = v[q];
-                px[q] = pr[q].x;
-                py[q] = pr[q].y;
-                pn[q] = pr[q].need;
-              }
-              have = true;
-            } else {
-#pragma unroll
-              for (int q = 0; q < E; ++q) probe_red(pr[q]);  // Alg.3 line 7
-            }
-          }
-        }
-        parity ^= 1u;
-        t += (ull)kRing * stride;
-      }
-      if (kDefer && have) {
-#pragma unroll
-        for (int q = 0; q < E; ++q) red_deferred(pv[q], px[q], py[q], pn[q], vd);
-      }
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < kRing; ++s) mbar_inval(bar0 + 8 * s);
-      }
-      __syncwarp();  // the ring's memory is the short tiles' staging next
-    } else {
+    {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;
     uint4 rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);
@@ -1107,10 +934,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
 }
 
 template <int E, int THREADS>
-static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cudaStream_t s) {
+static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, bool force_pos64, cudaStream_t s) {
   constexpr int SLOT = 32 * E + 2;
   constexpr size_t WARPS = THREADS / 32;
-  const bool pos32 = rk.nnz < (1ull << 32);  // every CSC position fits in 32 bits
+  const bool pos32 = rk.nnz < (1ull << 32) && !force_pos64;  // every CSC position fits in 32 bits
   const size_t staging = expand_stage_bytes<E, THREADS>(pos32);
   const size_t s_u_bytes = WARPS * SLOT * 4;
   // hot visited words per row segment: the relabeled prefix, as far as shared memory allows
@@ -1123,13 +950,7 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   // The hot copy fills the shared memory up to kSmemTarget in all: a larger carve-out costs L1
   // capacity, which holds the in-flight row loads and probes (measured at s26, peak level:
   // 162 KB of shared memory 3.67 ms, 178 KB 4.28 ms, 210 KB 6.9 ms).
-  static long env_kb = -1;
-  if (env_kb < 0) {  // tuning knob for experiments: BFS200_HOT_KB (hot copy size, overrides the target)
-    const char* env = getenv("BFS200_HOT_KB");
-    env_kb = (env && atoi(env) > 0) ? atoi(env) : 0;
-  }
-  const size_t hot_smem = env_kb ? (size_t)env_kb * 1024
-                                 : (kSmemTarget > staging + 16 + 64 ? kSmemTarget - staging - 16 - 64 : 4);
+  const size_t hot_smem = kSmemTarget > staging + 16 + 64 ? kSmemTarget - staging - 16 - 64 : 4;
   const uint64_t budget = hot_smem < kSmemBudget - staging - 16 ? hot_smem : kSmemBudget - staging - 16;
   const uint64_t cap = budget / 4 / (uint64_t)g.C - 1;  // + one sentinel word per segment
   if (hw > cap) hw = cap;
@@ -1138,17 +959,9 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
   // P1 levels keep s_u at the end of the region and (mode 3) at least the C sentinels before it
   if (region < s_u_bytes + (size_t)g.C * 4) region = s_u_bytes + (size_t)g.C * 4;
   const size_t smem = staging + region + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_expand<E, THREADS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    cudaFuncSetAttribute(k_expand<E, THREADS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    cudaFuncSetAttribute(k_expand<E, THREADS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    cudaFuncSetAttribute(k_expand<E, THREADS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    attr = true;
-  }
   auto kern = g.C == 1 ? (pos32 ? k_expand<E, THREADS, true, true> : k_expand<E, THREADS, true, false>)
                        : (pos32 ? k_expand<E, THREADS, false, true> : k_expand<E, THREADS, false, false>);
-  kern<<<num_sms(), THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vd,
+  kern<<<g.nsm, THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vd,
                                         rk.pmin, rk.inv_col, (uint32_t)hw, g.C, g.words_block(), blog,
                                         (uint32_t)(region / 4));
   return cudaGetLastError();
@@ -1156,13 +969,28 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, cuda
 
 uint32_t expand_tile_edges(int E) { return 32u * (uint32_t)E; }
 
-cudaError_t launch_expand(const Geom& g, Rank& rk, int E, uint64_t hot_h, cudaStream_t s) {
+template <int E, int THREADS>
+static cudaError_t expand_attrs() {
+  const int b = (int)kSmemBudget;
+  cudaError_t e = cudaFuncSetAttribute(k_expand<E, THREADS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_expand<E, THREADS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_expand<E, THREADS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_expand<E, THREADS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  return e;
+}
+
+
+
+cudaError_t launch_expand(const Geom& g, Rank& rk, int E, uint64_t hot_h, bool force_pos64, cudaStream_t s) {
   switch (E) {
-    case 1: return launch_expand_t<1, 1024>(g, rk, hot_h, s);
-    case 2: return launch_expand_t<2, 1024>(g, rk, hot_h, s);
-    case 4: return launch_expand_t<4, 1024>(g, rk, hot_h, s);
-    case 8: return launch_expand_t<8, 1024>(g, rk, hot_h, s);
-    case 16: return launch_expand_t<16, 512>(g, rk, hot_h, s);
+    case 1: return launch_expand_t<1, 1024>(g, rk, hot_h, force_pos64, s);
+    case 2: return launch_expand_t<2, 1024>(g, rk, hot_h, force_pos64, s);
+    case 4: return launch_expand_t<4, 1024>(g, rk, hot_h, force_pos64, s);
+    case 8: return launch_expand_t<8, 1024>(g, rk, hot_h, force_pos64, s);
+    case 16: return launch_expand_t<16, 512>(g, rk, hot_h, force_pos64, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1390,7 +1218,7 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t nwords = g.nrows() / 32;
   const uint64_t nchunks = (nwords + 31) / 32;
   uint64_t grid = (nchunks + kParentThreads / 32 - 1) / (kParentThreads / 32);
-  const uint64_t cap = (uint64_t)num_sms();
+  const uint64_t cap = (uint64_t)g.nsm;
   if (grid > cap) grid = cap;
   int blog = -1;
   if (g.block && (g.block & (g.block - 1)) == 0) {
@@ -1401,16 +1229,25 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   if (hw > g.words_block()) hw = g.words_block();
   if (blog < 0) hw = 0;
   const size_t smem = (size_t)(kParentThreads / 32) * 1024 * 4 + (size_t)(g.R * hw > 4 ? g.R * hw : 4) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
-    attr = true;
-  }
   k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
                                                         rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
                                                         (uint32_t)hw, g.R, g.words_block(), blog,
                                                         g.C > 1 ? rk.fold_dst : nullptr);
   return cudaGetLastError();
+}
+
+// Per-device launch attributes (the opt-in shared-memory sizes of K1 and K4).  The attribute
+// belongs to the current device's context, so every graph sets it for its own device at creation
+// (no process-wide "already set" flag).
+cudaError_t kernels_init_device() {
+  cudaError_t e = expand_attrs<1, 1024>();
+  if (e == cudaSuccess) e = expand_attrs<2, 1024>();
+  if (e == cudaSuccess) e = expand_attrs<4, 1024>();
+  if (e == cudaSuccess) e = expand_attrs<8, 1024>();
+  if (e == cudaSuccess) e = expand_attrs<16, 512>();
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+  return e;
 }
 
 // ------------------------------------------------------------------ K2: frontier update
@@ -1494,7 +1331,7 @@ cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaSt
   const uint64_t W = g.words_block();
   uint64_t gx = (W + 255) / 256;
   // peer stores: each CTA ends with a system-scope fence, so a capped grid strides instead
-  const uint64_t cap = (uint64_t)num_sms() * 8 / (uint64_t)g.C;
+  const uint64_t cap = (uint64_t)g.nsm * 8 / (uint64_t)g.C;
   if (g.R > 1 && rk.exp_dst && gx > cap) gx = cap ? cap : 1;
   const dim3 grid((unsigned)gx, (unsigned)g.C);
   k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
@@ -1521,10 +1358,14 @@ __global__ void k_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal,
     ctrl->lvl_frontier[l] = fr;
     ctrl->lvl_edges[l] = ed;
   }
+  ctrl->sum_frontier += fr;
+  ctrl->sum_edges += ed;
   ctrl->nlev = l + 1;
   ctrl->lvl += 1;
   ctrl->total_new = total;
-  const bool done = total == 0 || l + 1 >= kMaxLevels;
+  // a BFS ends after at most nverts levels; per-level statistics are kept for the first
+  // kMaxLevels levels only (deeper graphs, e.g. long paths, keep iterating)
+  const bool done = total == 0;
   ctrl->done = done ? 1u : 0u;
   if (use_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
 }
@@ -1534,6 +1375,8 @@ __global__ void k_level_begin(LevelCtrl* ctrl) {
   ctrl->nlev = 0;
   ctrl->done = 0;
   ctrl->total_new = 0;
+  ctrl->sum_frontier = 0;
+  ctrl->sum_edges = 0;
 }
 
 cudaError_t launch_level_begin(LevelCtrl* ctrl, cudaStream_t s) {
@@ -1703,7 +1546,7 @@ __global__ void k_req_push(const uint32_t* req, uint32_t* const* __restrict__ ds
 
 cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t n = g.words_block() * g.C;
-  const uint64_t blocks = (n + 255) / 256, cap = (uint64_t)num_sms() * 8;
+  const uint64_t blocks = (n + 255) / 256, cap = (uint64_t)g.nsm * 8;
   k_req_push<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(rk.req, rk.reqin_dst, g.words_block(), g.C);
   return cudaGetLastError();
 }
@@ -1727,7 +1570,7 @@ __global__ void k_resp_copy(const uint32_t* resp, const uint32_t* off, uint32_t*
 cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s) {
   cudaError_t e = launch_resp_pack(g, rk, s);  // packed locally (coalesced), then one bulk copy per peer
   if (e != cudaSuccess) return e;
-  k_resp_copy<<<num_sms() * 4, 256, 0, s>>>(rk.resp, rk.off_in, rk.respin_dst, g.words_block(), g.block, g.C, rk.j);
+  k_resp_copy<<<g.nsm * 4, 256, 0, s>>>(rk.resp, rk.off_in, rk.respin_dst, g.words_block(), g.block, g.C, rk.j);
   return cudaGetLastError();
 }
 
@@ -1744,7 +1587,7 @@ __global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uin
 }
 
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, ull* out, cudaStream_t s) {
-  k_mcomp<<<num_sms() * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, rk.fwd_own, g.block,
+  k_mcomp<<<g.nsm * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, rk.fwd_own, g.block,
                                          out);
   return cudaGetLastError();
 }
@@ -1844,12 +1687,10 @@ __global__ void k_seg_popc(const uint32_t* __restrict__ bm, uint64_t W, ull* cnt
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + blockIdx.y, (ull)c);
 }
 
-static uint64_t g_list_launches = 0;  // kernels launched by the list-exchange launchers
-uint64_t list_kernel_launches() { return g_list_launches; }
 
-cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, ull* cnt, cudaStream_t s) {
+cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, ull* cnt, uint64_t* launches, cudaStream_t s) {
   if (!W || nseg <= 0) return cudaSuccess;
-  ++g_list_launches;
+  ++*launches;
   const uint64_t blocks = (W + 255) / 256;
   k_seg_popc<<<dim3((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)nseg), 256, 0, s>>>(bm, W, cnt);
   return cudaGetLastError();
@@ -1881,14 +1722,14 @@ size_t list_encode_tmp_bytes(uint64_t nwords) {
 }
 
 cudaError_t launch_list_encode(const uint32_t* bm, uint64_t W, int nseg, uint32_t* off, void* tmp, size_t tmp_bytes,
-                               uint32_t* list, uint64_t lstride, cudaStream_t s) {
+                               uint32_t* list, uint64_t lstride, int nsm, uint64_t* launches, cudaStream_t s) {
   const uint64_t nwords = W * (uint64_t)nseg;
   if (!nwords) return cudaSuccess;
   cub::TransformInputIterator<uint32_t, PopcOp, const uint32_t*> it(bm, PopcOp());
   cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, it, off, nwords, s);
   if (e != cudaSuccess) return e;
-  ++g_list_launches;
-  k_list_write<<<num_sms() * 8, 256, 0, s>>>(bm, off, W, nwords, lstride, list);
+  ++*launches;
+  k_list_write<<<nsm * 8, 256, 0, s>>>(bm, off, W, nwords, lstride, list);
   return cudaGetLastError();
 }
 
@@ -1899,11 +1740,12 @@ __global__ void k_list_scatter(const uint32_t* __restrict__ list, uint64_t n, ui
   }
 }
 
-cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, cudaStream_t s) {
+cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, int nsm, uint64_t* launches,
+                               cudaStream_t s) {
   if (!n) return cudaSuccess;
-  ++g_list_launches;
+  ++*launches;
   const uint64_t blocks = (n + 255) / 256;
-  k_list_scatter<<<(unsigned)(blocks < (uint64_t)num_sms() * 8 ? blocks : (uint64_t)num_sms() * 8), 256, 0, s>>>(
+  k_list_scatter<<<(unsigned)(blocks < (uint64_t)nsm * 8 ? blocks : (uint64_t)nsm * 8), 256, 0, s>>>(
       list, n, bm);
   return cudaGetLastError();
 }

@@ -4,6 +4,9 @@
 
 namespace bfs200 {
 
+// Launch attributes of the hot-path kernels on the current device (call once per graph).
+cudaError_t kernels_init_device();
+
 // Alg.2 init lines P:334-343: reset per-search state of one rank and seed the root on its owner.
 cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s);
 
@@ -12,7 +15,8 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
 cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s);
 
 // K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
-cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, cudaStream_t s);
+cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, bool force_pos64,
+                          cudaStream_t s);
 uint32_t expand_tile_edges(int edges_per_thread);
 size_t seg_scan_tmp_bytes(uint64_t nseg);
 
@@ -45,12 +49,13 @@ cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned l
 // List exchange (opts.exchange): per-segment set-bit counts (added into cnt[k]),
 // bitmap segments -> ascending local index lists (list segment k at k*lstride), and lists -> bits
 // (OR into a zeroed bitmap segment).
-cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, unsigned long long* cnt, cudaStream_t s);
+cudaError_t launch_seg_popc(const uint32_t* bm, uint64_t W, int nseg, unsigned long long* cnt, uint64_t* launches,
+                            cudaStream_t s);
 size_t list_encode_tmp_bytes(uint64_t nwords);
 cudaError_t launch_list_encode(const uint32_t* bm, uint64_t W, int nseg, uint32_t* off, void* tmp, size_t tmp_bytes,
-                               uint32_t* list, uint64_t lstride, cudaStream_t s);
-cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, cudaStream_t s);
-uint64_t list_kernel_launches();  // running count of the three launchers' kernels (process-wide)
+                               uint32_t* list, uint64_t lstride, int nsm, uint64_t* launches, cudaStream_t s);
+cudaError_t launch_list_scatter(const uint32_t* list, uint64_t n, uint32_t* bm, int nsm, uint64_t* launches,
+                               cudaStream_t s);
 
 // Peer exchange (opts.peer_exchange): cross-GPU flag barrier over NVLink peer memory (optionally
 // summing the ranks' new-vertex counts into info->newv), and the root bit for column peers.

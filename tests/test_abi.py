@@ -42,9 +42,9 @@ def test_struct_layout_matches_header(L):
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(bfs_comm), sizeof(bfs_opts), sizeof(bfs_info), sizeof(bfs_stats),
          sizeof(bfs_level_record));
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", offsetof(bfs_info, nout), offsetof(bfs_stats, bytes_exchanged),
          offsetof(bfs_level_record, edges), offsetof(bfs_opts, exchange), offsetof(bfs_stats, list_messages),
-         offsetof(bfs_stats, kernel_launches), offsetof(bfs_opts, peer_exchange));
+         offsetof(bfs_stats, kernel_launches), offsetof(bfs_opts, peer_exchange), offsetof(bfs_opts, debug_flags));
   return 0;
 }
 '''
@@ -59,7 +59,7 @@ int main(void) {
                          ctypes.sizeof(bfs.Stats), ctypes.sizeof(bfs.LevelRecord)]
     assert sizes[5:] == [bfs.Info.nout.offset, bfs.Stats.bytes_exchanged.offset, bfs.LevelRecord.edges.offset,
                          bfs.Opts.exchange.offset, bfs.Stats.list_messages.offset, bfs.Stats.kernel_launches.offset,
-                         bfs.Opts.peer_exchange.offset]
+                         bfs.Opts.peer_exchange.offset, bfs.Opts.debug_flags.offset]
 
 
 def test_strerror_and_null_args(L):
@@ -77,6 +77,9 @@ def test_strerror_and_null_args(L):
     o = bfs.make_opts(edges_per_thread=3)
     assert L.bfs_graph_create(None, None, 0, 8, 1, 1, None, ctypes.byref(o), ctypes.byref(out)) == bfs.BFS_EINVAL
     assert b"edges_per_thread" in L.bfs_last_error()
+    o = bfs.make_opts(debug_flags=2)  # unknown debug flag
+    assert L.bfs_graph_create(None, None, 0, 8, 1, 1, None, ctypes.byref(o), ctypes.byref(out)) == bfs.BFS_EINVAL
+    assert L.bfs_gather(None, None, None, None, None) == bfs.BFS_EINVAL
 
 
 def test_product_does_not_import_oracle():

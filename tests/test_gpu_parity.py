@@ -269,32 +269,103 @@ def test_device_generator_matches_host(bfs):
         assert np.array_equal(dd.cpu().view(torch.int64).numpy().view(np.uint64), hd)
 
 
+# ---------------------------------------------------------------- the kernel variants the bench runs
+K_HOT_MIN_EDGES = 1 << 22  # kernels.cu kHotMinEdges: P2 levels below it skip the shared-memory hot copy
+
+
+@pytest.mark.parametrize("scale,grid", [(22, (1, 2)), (23, (2, 2))])
+def test_multi_column_hot_path(bfs, scale, grid):
+    """C > 1 grids at sizes whose peak levels exceed kHotMinEdges per rank, so K1 runs the
+    multi-segment hot-copy lookup (probe_segs) that the N > 1 bench configurations time; the
+    first root runs the host-driven level loop, later roots the CUDA-graph loop.  Bit-exact
+    level[] / parent[] / m_comp against the oracle."""
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    og = oracle.Graph(n, s, d)
+    g = make_graph(bfs, s, d, n, *grid)
+    roots = inputs.sample_roots(n, 4, inputs.nonisolated_mask(n, s, d))
+    for r in roots:
+        check_root(g, og, r, n)
+    # the per-rank peak level of this graph is above the hot-copy threshold (loopback level
+    # records sum the R*C local ranks)
+    g.set_opts(bfs.make_opts(edges_per_thread=4, phase_timing=True))
+    g.run(roots[0])
+    peak = max(x.edges for x in g.level_times())
+    assert peak / (grid[0] * grid[1]) > 2 * K_HOT_MIN_EDGES, peak
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (1, 2), (2, 2)])
+def test_pos64_variant(bfs, grid):
+    """The 64-bit staged-position K1 variant (used when a rank holds >= 2^32 CSC entries),
+    forced on a small graph with the test-only BFS_DEBUG_POS64 flag: bit-exact."""
+    scale = 16
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    og = oracle.Graph(n, s, d)
+    g = make_graph(bfs, s, d, n, *grid)
+    g.set_opts(bfs.make_opts(edges_per_thread=4, debug_flags=bfs.DEBUG_POS64))
+    for r in inputs.sample_roots(n, 6, inputs.nonisolated_mask(n, s, d)):
+        check_root(g, og, r, n)
+
+
+def test_deeper_than_level_records(bfs):
+    """A path of 5000 vertices: 5000 levels, more than the 4096 per-level records kept; the
+    BFS runs to the end (graph loop and host loop) and stats cover every level."""
+    n = 5000
+    t = np.stack([np.arange(n - 1, dtype=np.uint64), np.arange(1, n, dtype=np.uint64)], 1)
+    og = oracle.Graph(n, t[:, 0], t[:, 1])
+    g = make_graph(bfs, t[:, 0], t[:, 1], n, 1, 2)
+    for r in (0, 0, n - 1):  # first run host loop, then the CUDA-graph loop
+        check_root(g, og, r, n)
+    st = g.run(0)
+    assert st.nlevels == n and st.edges_scanned == 2 * (n - 1)  # n - 1 discovering levels + the empty one
+    g.set_opts(bfs.make_opts(edges_per_thread=4, phase_timing=True))
+    check_root(g, og, 0, n)
+    assert len(g.level_times(max_levels=8192)) == 4096
+
+
+def test_gather_loopback(bfs):
+    scale = 12
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    g = make_graph(bfs, s, d, n, 2, 2)
+    r = inputs.sample_roots(n, 1, inputs.nonisolated_mask(n, s, d))[0]
+    lv, pa = g.bfs(r)
+    la = np.full(g.info.npad, 7, dtype=np.int32)
+    pad = torch.full((g.info.npad,), 7, dtype=torch.int64, device="cuda")
+    g.gather(pa, lv, pad, la)
+    assert np.array_equal(la, lv) and np.array_equal(pad.cpu().numpy(), pa)
+
+
 # ---------------------------------------------------------------- full size (bench config)
 def test_s26_bench_config_graph500_valid(bfs):
-    """s26 1x1 (configs[2], the bench workload): device-generated graph, bench launch options;
-    host regenerates the identical tuples and the oracle's Graph500 validator checks V1-V6."""
-    import psutil
-    if psutil.virtual_memory().available < 48 << 30:
-        pytest.skip("needs ~48 GB host RAM for the s26 tuple list")
+    """s26 1x1 (configs[2], the bench workload): device-generated graph, bench launch options,
+    three roots (the first runs the host-driven level loop, the others the CUDA-graph loop the
+    bench times).  The oracle's streaming Graph500 validator regenerates the tuples from the
+    seed chunk by chunk and checks V1-V6 (equivalent to bit-exact equality with the oracle,
+    SURVEY.md §8(c)) and m_comp."""
     scale = 26
     n = 1 << scale
+    M = inputs.num_tuples(scale)
     ds, dd = inputs.generate_device(scale)
     g = bfs.Graph(ds, dd, n, 1, 1, opts=bfs.make_opts(edges_per_thread=4))
     del ds, dd
     torch.cuda.empty_cache()
-    hs, hd = inputs.generate(scale)
     roots = []
     t = 0
-    while len(roots) < 1:  # one root: the streaming validator takes ~2 min at s26
+    while len(roots) < 3:
         v = inputs.root_candidate(inputs.ROOT_SEED, t, n)
         t += 1
         if v not in roots and g.degree(v) > 0:
             roots.append(v)
+    step = 1 << 26
     for r in roots:
         lv, pa = g.bfs(r)
-        mask = oracle.validate(n, hs, hd, r, lv[:n], pa[:n])
+        mc = g.mcomp()
+        chunks = (inputs.generate(scale, k0=k, count=min(step, M - k)) for k in range(0, M, step))
+        mask, omc = oracle.validate_stream(n, r, lv[:n], pa[:n], chunks)
         assert mask == 0, oracle.failed_names(mask)
-        assert g.mcomp() == int(np.count_nonzero(lv[hs] >= 0))
+        assert mc == omc
 
 
 def test_unaligned_device_outputs(bfs):

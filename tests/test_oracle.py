@@ -240,47 +240,100 @@ def test_validator_accepts_oracle():
     assert oracle.validate(n, s, d, r, lv, pa) == 0
 
 
-def test_validator_fault_injection():
+def _fault_cases():
+    """(label, level, parent, check) for each invariant: check(mask) says what must fail."""
     n, s, d, r, lv, pa = _kron_case()
     bit = lambda name: 1 << oracle.V_NAMES.index(name)
+    cases = []
     # V1: root parent wrong
     p2 = pa.copy(); p2[r] = (r + 1) % n
-    assert oracle.validate(n, s, d, r, lv, p2) & bit("V1 root")
-    # V6: a non-minimal but valid parent (pick a vertex with >= 2 candidates)
+    cases.append(("V1", lv, p2, lambda m: m & bit("V1 root")))
+    # V6: a non-minimal but valid parent (pick a vertex with >= 2 candidates): ONLY V6 fails
     keep = s != d
     a = np.concatenate([s[keep], d[keep]]).astype(np.int64)
     b = np.concatenate([d[keep], s[keep]]).astype(np.int64)
     up = (lv[a] >= 0) & (lv[b] == lv[a] + 1)
     cand_a, cand_b = a[up], b[up]
-    done = False
     for v in np.unique(cand_b):
         cs = np.unique(cand_a[cand_b == v])
         if cs.size >= 2:
             p3 = pa.copy(); p3[v] = cs[-1]
-            m = oracle.validate(n, s, d, r, lv, p3)
-            assert m == bit("V6 min-rule"), oracle.failed_names(m)
-            done = True
+            cases.append(("V6", lv, p3, lambda m: m == bit("V6 min-rule")))
             break
-    assert done
+    else:
+        raise AssertionError("no vertex with two candidate parents")
     # V3: level off by one on a leaf-ish reached vertex
     v = int(np.flatnonzero(lv == lv.max())[0])
     l3 = lv.copy(); l3[v] += 1
-    assert oracle.validate(n, s, d, r, l3, pa) & bit("V3 level+1")
-    # V2: parent that is not a neighbour but sits one level up
-    v = int(np.flatnonzero(lv == 2)[0])
+    cases.append(("V3", l3, pa, lambda m: m & bit("V3 level+1")))
+    # V2: parent that is not a neighbour but sits one level up: ONLY V2 fails
+    # (a level-1 non-neighbour BELOW the true minimum parent, so the min rule V6 still holds)
+    l1 = np.flatnonzero(lv == 1)
+    v = max(np.flatnonzero(lv == 2).tolist(), key=lambda x: pa[x])
     nbrs = set(b[a == v].tolist())
-    fake = [u for u in np.flatnonzero(lv == 1) if u not in nbrs]
+    fake = [u for u in l1 if u not in nbrs and u < pa[v]]
     p4 = pa.copy(); p4[v] = fake[0]
-    assert oracle.validate(n, s, d, r, lv, p4) & bit("V2 tree-edge")
-    # V5: drop a reached vertex
+    cases.append(("V2", lv, p4, lambda m: m == bit("V2 tree-edge")))
+    # V5 alone (1): an unreached vertex whose parent is not -1 -- no other invariant looks at it
+    v = int(np.flatnonzero(lv < 0)[0])
+    p5 = pa.copy(); p5[v] = r
+    cases.append(("V5-unreached", lv, p5, lambda m: m == bit("V5 component")))
+    # V5 alone (2): a reached vertex whose parent id is out of range
+    v = int(np.flatnonzero(lv == 1)[0])
+    p5b = pa.copy(); p5b[v] = n
+    cases.append(("V5-range", lv, p5b, lambda m: m == bit("V5 component")))
+    # dropping a reached vertex breaks the component (V5) and the edge span (V4) together: the
+    # component half of V5 alone cannot fail (V1-V4 imply it: V4 closes the reached set under
+    # tuples, V1-V3 connect it to the root), so it is pinned together with V4
     v = int(np.flatnonzero(lv == lv.max())[0])
-    l5 = lv.copy(); p5 = pa.copy(); l5[v] = -1; p5[v] = -1
-    assert oracle.validate(n, s, d, r, l5, p5) & (bit("V5 component") | bit("V4 edge-span"))
+    l5 = lv.copy(); p5c = pa.copy(); l5[v] = -1; p5c[v] = -1
+    cases.append(("V5+V4", l5, p5c, lambda m: (m & bit("V5 component")) and (m & bit("V4 edge-span"))))
     # V4: a tuple spanning two levels
     l6 = lv.copy()
     v = int(np.flatnonzero(lv == 1)[0])
     l6[v] = 3
-    assert oracle.validate(n, s, d, r, l6, pa) & bit("V4 edge-span")
+    cases.append(("V4", l6, pa, lambda m: m & bit("V4 edge-span")))
+    return n, s, d, r, cases
+
+
+def test_validator_fault_injection():
+    n, s, d, r, cases = _fault_cases()
+    for label, lv, pa, check in cases:
+        m = oracle.validate(n, s, d, r, lv, pa)
+        assert check(m), (label, oracle.failed_names(m))
+
+
+@pytest.mark.parametrize("chunk", [7, 1000, None])
+def test_stream_validator_matches_oneshot(chunk):
+    """The streaming validator (oracle.c step 6, written separately) gives the same mask as
+    oracle_validate on every fault case and on valid trees, for any chunking of the tuples."""
+    n, s, d, r, cases = _fault_cases()
+    m_all = s.size
+    step = chunk or m_all
+    for label, lv, pa, check in cases + [("valid", *_kron_case()[4:], lambda m: m == 0)]:
+        one = oracle.validate(n, s, d, r, lv, pa)
+        assert check(one), label
+        mask, mc = oracle.validate_stream(n, r, lv, pa, ((s[k:k + step], d[k:k + step]) for k in range(0, m_all, step)))
+        assert mask == one, (label, oracle.failed_names(mask), oracle.failed_names(one))
+        if not mask & (1 << oracle.V_NAMES.index("V5 component")):  # else parent[] is unusable: no pass
+            assert mc == int(np.count_nonzero(lv[s] >= 0))
+
+
+@pytest.mark.parametrize("scale", [10, 13, 16])
+def test_stream_validator_regenerated_chunks(scale):
+    """Chunks regenerated from the seed (what the full-size GPU checks do) validate the oracle's
+    own trees, and m_comp matches the oracle's count."""
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    g = oracle.Graph(n, s, d)
+    M = inputs.num_tuples(scale)
+    step = M // 5 + 3
+    for r in inputs.sample_roots(n, 3, inputs.nonisolated_mask(n, s, d)):
+        lv, pa = g.bfs(r)
+        chunks = (inputs.generate(scale, k0=k, count=min(step, M - k)) for k in range(0, M, step))
+        mask, mc = oracle.validate_stream(n, r, lv, pa, chunks)
+        assert mask == 0, oracle.failed_names(mask)
+        assert mc == g.mcomp(lv)
 
 
 def test_isolated_and_out_of_range_root():
