@@ -10,7 +10,8 @@ N=1 runs configs[2] (scale 26, 1x1); N>1 (torchrun, one rank per GPU) runs weak 
 scale 26 + log2(N) on the grids 1x2, 2x2, 2x4 (configs[4]'s grid shapes).  TEPS_i = m_comp_i /
 t_i, t_i = max over ranks of the CUDA-event time of bfs_run on the library's
 stream; value = harmonic mean of the K timed steps in GTEPS.  L2 is flushed between
-steps (and the graph is > L2).  --impl reference times the CPU oracle on a bounded sample.
+steps (and the graph is > L2).  --impl reference times the CPU oracle (as it stands) on the
+same graph: one root per step, the roots spread over the host cores (one process each).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -31,7 +32,6 @@ sys.path.insert(0, ROOT)
 METRIC = "GTEPS (harmonic mean, 64 roots) Graph500 Kronecker ef16 at 1/2/4/8 B200"
 UNIT = "GTEPS"
 GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
-REF_SAMPLE_SCALE = 20  # oracle sample graph for --impl reference / cpu_baseline steps
 
 
 def hmean(xs):
@@ -101,23 +101,124 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def oracle_sample(steps: int, warmup: int, scale: int = REF_SAMPLE_SCALE):
-    """Time the CPU oracle (as it stands) on `steps` roots of a scale-`scale` Kronecker graph."""
-    import oracle
-    from paper_1408_1605_b200 import inputs
-    s, d = inputs.generate(scale)
-    n = 1 << scale
-    g = oracle.Graph(n, s, d)
-    roots = inputs.sample_roots(n, 64, lambda v: g.degree(v) > 0)
-    teps = []
-    for k in range(warmup + steps):
-        r = roots[k % len(roots)]
+# The oracle (oracle/oracle.c, serial) timed as it stands on the host cores: its adjacency is
+# built once (untimed, like GPU graph construction), then roots run one per process on separate
+# cores (forked workers share the adjacency copy-on-write); per root TEPS = m_comp / t with t the
+# BFS + min-parent pass (oracle steps 2-3), m_comp counted outside the timed region.
+_OG = None
+
+
+def _oracle_root(r):
+    t0 = time.perf_counter()
+    lv, _ = _OG.bfs(r)
+    t = time.perf_counter() - t0
+    return r, t, _OG.mcomp(lv)
+
+
+def cpu_info():
+    cores = len(os.sched_getaffinity(0))
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+class OracleLeg:
+    """Build the scale-S oracle adjacency (untimed), then time roots spread over the host cores."""
+
+    def __init__(self, scale: int, gen_threads: int = 0):
+        global _OG
+        import oracle
+        from paper_1408_1605_b200 import inputs
+        self.scale, self.n = scale, 1 << scale
         t0 = time.perf_counter()
-        lv, _ = g.bfs(r)
-        t = time.perf_counter() - t0
-        if k >= warmup:
-            teps.append(g.mcomp(lv) / t)
-    return hmean(teps) / 1e9, f"oracle BFS+parent pass, Kronecker scale {scale} ef16, {steps} roots (graph seed 1)"
+        if gen_threads:
+            os.environ["OMP_NUM_THREADS"] = str(gen_threads)
+        self.src, self.dst = inputs.generate(scale)
+        self.g = oracle.Graph(self.n, self.src, self.dst)
+        _OG = self.g
+        self.build_s = time.perf_counter() - t0
+
+    def roots(self, count):
+        from paper_1408_1605_b200 import inputs
+        return inputs.sample_roots(self.n, count, lambda v: self.g.degree(v) > 0)
+
+    def run(self, roots, procs):
+        import multiprocessing as mp
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_oracle_root, roots, chunksize=1)
+        return res, time.perf_counter() - t0
+
+
+def oracle_measure(scale: int, timed: int, warm: int = 0, gen_threads: int = 0):
+    """Harmonic-mean GTEPS of the oracle over `timed` roots of the scale-`scale` graph (the
+    first `timed` roots of the bench's root stream; `warm` further roots run alongside, untimed)."""
+    cores, model = cpu_info()
+    leg = OracleLeg(scale, gen_threads)
+    roots = leg.roots(timed + warm)
+    procs = max(1, min(cores, len(roots)))
+    res, wall = leg.run(roots, procs)
+    res = res[:timed]
+    teps = [mc / t for _, t, mc in res]
+    per_root_s = [t for _, t, _ in res]
+    return {"value": hmean(teps) / 1e9, "unit": UNIT, "cores": procs, "cores_available": cores, "cpu_model": model,
+            "kind": "oracle",
+            "sample": (f"oracle BFS + min-parent pass (oracle/oracle.c steps 2-3), Graph500 Kronecker scale {scale} "
+                       f"ef16 (graph seed 1), {timed} timed roots of root seed 2 (+{warm} untimed), one root per "
+                       f"process on {procs} of {cores} host cores, adjacency built once untimed "
+                       f"({leg.build_s:.0f} s)"),
+            "per_root_s": {"min": min(per_root_s), "max": max(per_root_s)},
+            "aggregate_gteps": sum(mc for _, _, mc in res) / wall / 1e9 if len(res) == len(roots) else None,
+            "wall_s": wall}
+
+
+def cpu_leg_main(args):
+    """Subprocess body of the cpu_baseline leg: build, print 'ready', wait for 'go' on stdin (the
+    GPU arm's timed regions are over), time the roots, print the result as one JSON line."""
+    cores, _ = cpu_info()
+    leg = OracleLeg(args.scale, gen_threads=4)
+    roots = leg.roots(args.cpu_roots)
+    print("ready", flush=True)
+    sys.stdin.readline()
+    procs = max(1, min(cores, len(roots)))
+    res, wall = leg.run(roots, procs)
+    teps = [mc / t for _, t, mc in res]
+    _, model = cpu_info()
+    print(json.dumps({"value": hmean(teps) / 1e9, "unit": UNIT, "cores": procs, "cores_available": cores,
+                      "cpu_model": model, "kind": "oracle",
+                      "sample": (f"oracle BFS + min-parent pass (oracle/oracle.c steps 2-3), Graph500 Kronecker "
+                                 f"scale {args.scale} ef16 (graph seed 1; the bench graph), the first {len(roots)} "
+                                 f"roots of root seed 2, one root per process on {procs} of {cores} host cores "
+                                 f"(forked workers sharing the adjacency, built once untimed in {leg.build_s:.0f} s)"),
+                      "per_root_s": {"min": min(r[1] for r in res), "max": max(r[1] for r in res)},
+                      "aggregate_gteps": sum(r[2] for r in res) / wall / 1e9, "wall_s": wall}), flush=True)
+
+
+def cpu_leg_start(scale: int, roots: int):
+    """Start the oracle leg in a subprocess: its untimed adjacency build overlaps the GPU work."""
+    return subprocess.Popen([sys.executable, os.path.abspath(__file__), "--cpu-leg", "--scale", str(scale),
+                             "--cpu-roots", str(roots)], stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+
+
+def cpu_leg_finish(proc):
+    try:
+        line = proc.stdout.readline()  # 'ready' (build done)
+        if line.strip() != "ready":
+            raise RuntimeError(f"oracle leg failed to build: {line!r}")
+        proc.stdin.write("go\n")
+        proc.stdin.flush()
+        out = proc.stdout.readline()
+        proc.wait(timeout=60)
+        return json.loads(out)
+    except Exception as e:  # reported, never fatal for the GPU line
+        proc.kill()
+        return {"value": None, "unit": UNIT, "kind": "oracle", "error": str(e)[:200]}
 
 
 def run_reference(args, rank, world):
@@ -125,12 +226,13 @@ def run_reference(args, rank, world):
         return
     cfg = workload_config(args, world)
     steps = max(1, args.steps)
-    v, sample = oracle_sample(steps, max(0, args.warmup))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic", "config": cfg,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    cb = oracle_measure(cfg["scale"], steps, max(0, args.warmup))
+    cfg = dict(cfg, roots=steps)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (seeded Graph500-style Kronecker, graph seed 1, root seed 2)",
+            "config": cfg, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -203,6 +305,11 @@ def run_ours(args, rank, world, local_rank):
     R, C = grid_of(args, world)
     n = 1 << scale
     M = inputs.num_tuples(scale)
+    # cpu_baseline (rank 0, N = 1): the oracle leg's untimed adjacency build overlaps the GPU work;
+    # its roots run after the GPU's timed regions
+    cpu_proc = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu_proc = cpu_leg_start(scale, min(16, cpu_info()[0]))
     # this rank's slice of the tuple list, generated in HBM
     k0 = M * rank // world
     k1 = M * (rank + 1) // world
@@ -238,6 +345,7 @@ def run_ours(args, rank, world, local_rank):
     # 64 timed roots + W warm-up roots: degree >= 1, distinct, root stream of seed 2
     roots = sample_roots_collective(n, 64 + args.warmup, g.degree)
     timed_roots = roots[:64]
+    cfg["roots"] = min(args.steps, len(timed_roots))  # distinct roots actually timed
     warm_roots = roots[64:] or roots[:1]
     parent = torch.empty(info.nout, dtype=torch.int64, device=dev)
     level = torch.empty(info.nout, dtype=torch.int32, device=dev)
@@ -272,7 +380,14 @@ def run_ours(args, rank, world, local_rank):
     value = hmean(teps) / 1e9
 
     # phase-timed replay of the same roots (host-driven level loop, CUDA events around every phase)
+    # Algorithmic bytes of level L: B_L = 4 E_L + 40 F_L -- a 4-B `row` entry per
+    # scanned edge, and per frontier column 16 B of `col` offsets + 24 B of frontier list / scan
+    # entries written and read.
+    def alg_bytes(rec):
+        return 4.0 * rec.edges + 40.0 * rec.frontier
+
     exp_bytes, exp_ms, lvl_tot, replay_ms = 0.0, 0.0, 0, 0.0
+    pk = {"bytes": 0.0, "k1_ms": 0.0, "level_ms": 0.0, "edges": 0}
     tail = {"finalize": 0.0, "resolve": 0.0}
     phase = {"expand_comm": 0.0, "scan": 0.0, "expand": 0.0, "parent": 0.0, "fold_comm": 0.0, "update": 0.0,
              "allreduce": 0.0}
@@ -295,11 +410,45 @@ def run_ours(args, rank, world, local_rank):
             for rec in recs:
                 for key in phase:
                     phase[key] += getattr(rec, key)
-                # algorithmic bytes of one expansion launch: 4 B row entry per scanned edge +
-                # 20 B per frontier column (list 4 + cumul 8 + row offset 8)
-                exp_bytes += 4.0 * rec.edges + 20.0 * rec.frontier
+                exp_bytes += alg_bytes(rec)
                 exp_ms += rec.expand
+            top = max(recs, key=lambda x: x.edges)  # the peak level of this root
+            pk["bytes"] += alg_bytes(top)
+            pk["k1_ms"] += top.expand
+            pk["level_ms"] += top.scan + top.expand + top.parent + top.update
+            pk["edges"] += top.edges
         g.set_opts(opts)
+
+    # NVLink (N > 1): peer bandwidth measured in-run at the per-level message size (one bitmap
+    # segment, block/8 bytes, to every other rank: all-to-all over the world), against the bytes
+    # the per-level exchanges move (bfs_stats.bytes_exchanged)
+    nvl = None
+    if world > 1:
+        msg = int(info.block) // 8
+        a2a_in = torch.zeros(world * msg, dtype=torch.uint8, device=dev)
+        a2a_out = torch.empty_like(a2a_in)
+        for _ in range(3):
+            dist.all_to_all_single(a2a_out, a2a_in)
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        reps = 10
+        for _ in range(reps):
+            dist.all_to_all_single(a2a_out, a2a_in)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t_a2a = max_over_ranks(ev0.elapsed_time(ev1) / reps)
+        bw_nvl = (world - 1) * msg / (t_a2a * 1e-3) / 1e9  # GB/s sent per GPU
+        b_nvl = xbytes / max(1, args.steps) / max(1, int(info.nlocal))
+        step_s = sum(times) / len(times) * 1e-3
+        nvl = {"bw_measured_gbs": bw_nvl, "msg_bytes": msg, "how": "torch.distributed all_to_all_single (NCCL), "
+               "block/8 bytes per peer, 10 reps after 3 warm-up, max over ranks",
+               "bytes_per_step_per_gpu": b_nvl, "achieved_gbs": b_nvl / step_s / 1e9,
+               "frac": (b_nvl / step_s / 1e9) / bw_nvl if bw_nvl else None,
+               "roofline_ms_per_step": b_nvl / (bw_nvl * 1e9) * 1e3 if bw_nvl else None,
+               "note": "per-level fold/expand bitmaps only (the end-of-search resolution is excluded); the "
+                       "exchange is fused into K4/K2 as NVLink peer stores, so it overlaps the kernels"}
+        del a2a_in, a2a_out
 
     # e2e: same metric through the C ABI with a HOST output buffer (D2H inside the timed region).
     # The result read back is the BFS tree (parent array, Graph500's output); levels are optional
@@ -320,13 +469,15 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = measured_peaks()
     per_rank_exp_ms = exp_ms  # phase times are per rank; expansion kernel of this rank
     achieved = (exp_bytes / 1e9) / (per_rank_exp_ms * 1e-3) if per_rank_exp_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "expand_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    peak_levels = None
+    if pk["k1_ms"] > 0:
+        a_k1 = pk["bytes"] / 1e9 / (pk["k1_ms"] * 1e-3)
+        a_lv = pk["bytes"] / 1e9 / (pk["level_ms"] * 1e-3)
+        peak_levels = {"alg_bytes_per_step": pk["bytes"] / args.steps, "edges_per_step": pk["edges"] / args.steps,
+                       "k1_ms_per_step": pk["k1_ms"] / args.steps, "level_ms_per_step": pk["level_ms"] / args.steps,
+                       "k1_gbs": a_k1, "k1_frac": a_k1 / peak, "level_gbs": a_lv, "level_frac": a_lv / peak,
+                       "definition": "per root the level with the most scanned edges; B_L = 4 E_L + 40 F_L; "
+                                     "k1 = k_expand time, level = K3 scan + K1 expand + K4 parent + K2 update"}
     step_ms = sum(times) / len(times)
     g.close()
     if rank != 0:
@@ -343,13 +494,18 @@ def run_ours(args, rank, world, local_rank):
         "exchange": {"mode": args.exchange, "bytes_per_step_rank0": xbytes / max(1, args.steps),
                      "list_messages_per_step_rank0": xlists / max(1, args.steps)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "traffic_note": "not measured in-run (needs ncu); the ncu capture of this config's peak "
+                                     "k_expand launch is in profiles/ (DRAM vs algorithmic bytes)",
                      "kernel": "k_expand (frontier expansion, Alg.3)", "peak_kind": peak_kind,
                      "alg_bytes_per_step": exp_bytes / max(1, args.steps),
+                     "alg_bytes_definition": "sum over levels of 4 E_L + 40 F_L (SURVEY.md §8(d))",
                      "kernel_ms_per_step": per_rank_exp_ms / max(1, args.steps),
                      "kernel_share_of_step": per_rank_exp_ms / replay_ms if replay_ms else None,
+                     "peak_levels": peak_levels,
                      "timing": "CUDA events around every k_expand launch in a phase-timed replay of the K "
-                               "timed roots (the timed steps run the level loop as one CUDA graph)"},
+                               "timed roots (the timed steps run the level loop as one CUDA graph); rank 0"},
+        "nvlink": nvl,
         "phase_ms_per_step": {**{k: v / max(1, args.steps) for k, v in phase.items()},
                               **{k: v / max(1, args.steps) for k, v in tail.items()}},
         "levels_per_step": lvl_tot / max(1, args.steps),
@@ -362,10 +518,8 @@ def run_ours(args, rank, world, local_rank):
         "construction": {"generate_s": t_gen, "build_s": t_build,
                          "tuples_per_s": M / (t_gen + t_build) if t_gen + t_build > 0 else None},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        ns = int(os.environ.get("BENCH_CPU_ROOTS", "4"))
-        v, sample = oracle_sample(ns, 0)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+    if world == 1 and cpu_proc is not None:
+        line["cpu_baseline"] = cpu_leg_finish(cpu_proc)
     print(json.dumps(line), flush=True)
 
 
@@ -385,6 +539,8 @@ def main():
                          "or NCCL collectives")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase-timing", action="store_true", help="(diagnostic) no per-phase events")
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)  # cpu_baseline subprocess
+    ap.add_argument("--cpu-roots", type=int, default=16, help=argparse.SUPPRESS)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -392,6 +548,9 @@ def main():
     if world != args.gpus and world == 1 and args.gpus > 1:
         print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with {args.gpus} ranks"}), flush=True)
         sys.exit(2)
+    if args.cpu_leg:
+        cpu_leg_main(args)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
