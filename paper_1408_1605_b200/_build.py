@@ -94,6 +94,31 @@ def build_bfs(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines, force: bool = False) -> str:
+    """An experiment build of the same library with extra -D flags (A/B runs through BFS200_LIB);
+    build/variants/lib<name>.so.  Never loaded unless BFS200_LIB points at it."""
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(INCLUDE, "*.h")))
+    vdir = os.path.join(BUILD_DIR, "variants", name)
+    out = os.path.join(BUILD_DIR, "variants", f"lib{name}.so")
+    if not force and not _stale(out, srcs + hdrs):
+        return out
+    os.makedirs(vdir, exist_ok=True)
+    inc, lib = nccl_dirs()
+    dflags = [f"-D{d}" for d in defines]
+    objs, jobs = [], []
+    for s in srcs:
+        o = os.path.join(vdir, os.path.basename(s)[:-3] + ".o")
+        objs.append(o)
+        jobs.append(([nvcc(), *ARCH, *NVCC_FLAGS, *dflags, "-I", INCLUDE, "-I", inc, "-c", s, "-o", o], o + ".log"))
+    with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+        list(ex.map(lambda a: _run(*a), jobs))
+    _run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}",
+          "-lcudart"], os.path.join(vdir, "link.log"))
+    return out
+
+
 def build_kron_dev(force: bool = False) -> str:
     src = os.path.join(PKG, "inputs", "kron_dev.cu")
     hdr = os.path.join(PKG, "inputs", "kron_gen.h")

@@ -27,7 +27,7 @@ struct LevelInfo {
   unsigned long long newv;    // vertices discovered by the update (this rank)
   unsigned long long mode;    // parent claim of this level: 1 = atomicMin in the expansion (P1),
                               // 2 = CSR scan of the discovered rows (P2), 3 = P1 with the
-                              // discovered words derived from pmin; see k_level_info
+                              // discovered words derived from pmin; see k_seg_scan
   unsigned long long nlong;   // hub columns whose long-tile records are written by k_tile_fill
   unsigned long long sedges;  // edges of the short columns = cumul[n]
   unsigned long long nA;      // long-column tiles (tileA records)
@@ -103,8 +103,6 @@ struct Rank {
   uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
   void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
   void* seg_off = nullptr;               // [nseg+1] their exclusive scan (seg_off[nseg] = level total)
-  void* seg_tmp = nullptr;               // CUB temp of the segment scan
-  size_t seg_tmp_bytes = 0;
   uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution

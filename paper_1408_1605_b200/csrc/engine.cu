@@ -198,8 +198,6 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.seg_tot, (nseg + 1) * 32);
   AL(rk.seg_off, (nseg + 1) * 32);
   CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
-  rk.seg_tmp_bytes = seg_scan_tmp_bytes(nseg);
-  AL(rk.seg_tmp, rk.seg_tmp_bytes);
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
   AL(rk.scratch, 64 * 8);

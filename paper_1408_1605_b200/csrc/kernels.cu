@@ -126,12 +126,6 @@ struct SegTot {
   ull ls;           // long edges
 };
 static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
-struct SegAdd {
-  __device__ __forceinline__ SegTot operator()(const SegTot& a, const SegTot& b) const {
-    return SegTot{a.cs + b.cs, a.na + b.na, a.nh + b.nh, 0u, a.ss + b.ss, a.ls + b.ls};
-  }
-};
-
 // Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
 // chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
@@ -229,15 +223,79 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
 #endif
 constexpr bool kBlind3 = BFS200_BLIND3;
 
-// Parent-claim mode thresholds (k_level_info; measured at s26): P2 when a row's
+// Parent-claim mode thresholds (k_seg_scan; measured at s26): P2 when a row's
 // expected CSR scan is <= kP2Factor entries; mode 3 when the P1 candidate edges are >= rows / kM3Factor.
 constexpr ull kP2Factor = 8;
 constexpr ull kM3Factor = 4;
 
-// level totals from the segment scan (seg_off[nseg] = sum over all segments); resets counters
-__global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* info, ull* cumul, ull nnz,
-                             ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
-  const SegTot c = seg_off[nseg];
+// K3 scan of the per-segment totals, one CTA (the totals are few: one per 4096 columns), fused
+// with the level bookkeeping: seg_off[k] = exclusive scan of seg_tot (seg_off[nseg] = the level's
+// totals), then the per-level counters and the parent-claim mode.  Pass k scans segments
+// [1024k, 1024k + 1024): warp inclusive scans by shuffles, the 32 warp totals scanned by warp 0
+// through shared memory, a running carry; the next pass's totals are loaded during this one.
+constexpr int kSegScanThreads = 1024;
+struct SegAcc {  // the scanned fields (pad is never summed)
+  unsigned cs, na, nh;
+  ull ss, ls;
+};
+__device__ __forceinline__ SegAcc seg_add(const SegAcc& a, const SegAcc& b) {
+  return SegAcc{a.cs + b.cs, a.na + b.na, a.nh + b.nh, a.ss + b.ss, a.ls + b.ls};
+}
+__device__ __forceinline__ SegAcc seg_sub(const SegAcc& a, const SegAcc& b) {
+  return SegAcc{a.cs - b.cs, a.na - b.na, a.nh - b.nh, a.ss - b.ss, a.ls - b.ls};
+}
+__device__ __forceinline__ SegAcc seg_shfl_up(const SegAcc& a, int d) {
+  return SegAcc{__shfl_up_sync(0xFFFFFFFFu, a.cs, d), __shfl_up_sync(0xFFFFFFFFu, a.na, d),
+                __shfl_up_sync(0xFFFFFFFFu, a.nh, d), __shfl_up_sync(0xFFFFFFFFu, a.ss, d),
+                __shfl_up_sync(0xFFFFFFFFu, a.ls, d)};
+}
+__device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t n) {
+  if (k >= n) return SegAcc{0u, 0u, 0u, 0ull, 0ull};
+  const SegTot t = p[k];
+  return SegAcc{t.cs, t.na, t.nh, t.ss, t.ls};
+}
+
+__global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
+                                                               SegTot* seg_off, LevelInfo* info, ull* cumul, ull nnz,
+                                                               ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
+  __shared__ SegAcc s_warp[kSegScanThreads / 32];
+  __shared__ SegAcc s_carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  SegAcc carry{0u, 0u, 0u, 0ull, 0ull};
+  SegAcc cur = seg_load(seg_tot, threadIdx.x, nseg);
+  for (uint64_t base = 0; base < nseg; base += kSegScanThreads) {
+    const SegAcc nxt = seg_load(seg_tot, base + kSegScanThreads + threadIdx.x, nseg);  // in flight
+    SegAcc inc = cur;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const SegAcc y = seg_shfl_up(inc, d);
+      if (lane >= d) inc = seg_add(inc, y);
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const SegAcc w = s_warp[lane];
+      SegAcc wi = w;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const SegAcc y = seg_shfl_up(wi, d);
+        if (lane >= d) wi = seg_add(wi, y);
+      }
+      s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
+      if (lane == 31) s_carry = wi;   // the pass total
+    }
+    __syncthreads();
+    const SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, cur)));
+    const uint64_t k = base + threadIdx.x;
+    if (k < nseg) seg_off[k] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
+    carry = seg_add(carry, s_carry);
+    __syncthreads();  // s_warp / s_carry are rewritten by the next pass
+    cur = nxt;
+  }
+  if (threadIdx.x != 0) return;
+  const SegAcc c = carry;
+  seg_off[nseg] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
+  // level totals; resets the per-level counters
   info->n = c.cs;
   info->sedges = c.ss;
   info->nA = c.na;
@@ -263,13 +321,6 @@ __global__ void k_level_info(const SegTot* seg_off, uint64_t nseg, LevelInfo* in
   info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
   info->nlongcols = 0;
   cumul[c.cs] = c.ss;
-}
-
-size_t seg_scan_tmp_bytes(uint64_t nseg) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const SegTot*)nullptr, (SegTot*)nullptr, SegAdd(),
-                                 SegTot{0u, 0u, 0u, 0u, 0ull, 0ull}, (uint64_t)nseg + 1);
-  return bytes;
 }
 
 // Emit pass: same word ownership.  Sparse chunks (< 96 set bits in 32 words): each lane totals
@@ -481,11 +532,9 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   SegTot* st = static_cast<SegTot*>(rk.seg_tot);
   SegTot* so = static_cast<SegTot*>(rk.seg_off);
   k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
-  // exclusive scan over nseg+1 segment totals (st[nseg] stays zero) -> so[nseg] = level total
-  cub::DeviceScan::ExclusiveScan(rk.seg_tmp, rk.seg_tmp_bytes, st, so, SegAdd(), SegTot{0u, 0u, 0u, 0u, 0ull, 0ull},
-                                 (uint64_t)nseg + 1, s);
-  k_level_info<<<1, 1, 0, s>>>(so, nseg, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows, kM3Factor,
-                               (ull)g.nrows());
+  // exclusive scan of the nseg segment totals (so[nseg] = level total) + the level's counters
+  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(st, nseg, so, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
+                                          kM3Factor, (ull)g.nrows());
   k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
@@ -635,6 +684,142 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
   }
 }
 
+// Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
+// keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
+// word address from v (two instructions instead of three live registers per row).
+__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
+                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd) {
+  asm("{\n"
+      " .reg .pred pok, pn;\n"
+      " .reg .b32 wi, hi, hv, m;\n"
+      " .reg .b64 a;\n"
+      " setp.lt.u32 pok, %4, %5;\n"
+      " shr.b32 wi, %3, 5;\n"
+      " min.u32 hi, wi, %6;\n"
+      " shl.b32 hi, hi, 2;\n"
+      " add.u32 hi, hi, %7;\n"
+      " ld.shared.u32 hv, [hi];\n"
+      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " and.b32 hv, hv, m;\n"
+      " setp.eq.and.b32 pn, hv, 0, pok;\n"
+      " mad.wide.u32 a, wi, 8, %8;\n"
+      " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
+      "}"
+      : "=r"(x), "=r"(y), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
+}
+__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
+                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd, int bl,
+                                            uint32_t bmask) {
+  asm("{\n"
+      " .reg .pred pok, pn;\n"
+      " .reg .b32 wi, hi, hv, sg, off, m;\n"
+      " .reg .b64 a;\n"
+      " setp.lt.u32 pok, %4, %5;\n"
+      " shr.b32 wi, %3, 5;\n"
+      " shr.b32 sg, %3, %9;\n"
+      " and.b32 off, %3, %10;\n"
+      " shr.b32 off, off, 5;\n"
+      " min.u32 off, off, %6;\n"
+      " add.u32 hv, %6, 1;\n"
+      " mad.lo.u32 hi, sg, hv, off;\n"
+      " selp.u32 hi, hi, %6, pok;\n"
+      " shl.b32 hi, hi, 2;\n"
+      " add.u32 hi, hi, %7;\n"
+      " ld.shared.u32 hv, [hi];\n"
+      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " and.b32 hv, hv, m;\n"
+      " setp.eq.and.b32 pn, hv, 0, pok;\n"
+      " mad.wide.u32 a, wi, 8, %8;\n"
+      " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
+      "}"
+      : "=r"(x), "=r"(y), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+}
+__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
+  asm volatile("{\n"
+               " .reg .pred pn, pr;\n"
+               " .reg .b32 t, m, wi;\n"
+               " .reg .b64 a;\n"
+               " setp.ne.b32 pn, %3, 0;\n"
+               " shf.l.wrap.b32 m, 0, 1, %0;\n"
+               " lop3.b32 t, %1, %2, m, 0xa8;\n"
+               " setp.eq.and.b32 pr, t, 0, pn;\n"
+               " shr.b32 wi, %0, 5;\n"
+               " mad.wide.u32 a, wi, 8, %4;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
+               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
+}
+
+// Long-column tiles of a P2 level, software-pipelined (the hot loop of the peak level).  A warp
+// walks its tiles q = 0, 1, ... (tile id t0 + q*stride) through NS slots: in phase q it issues the
+// `row` loads of tile q+NS-1 (so every tile's rows have NS-1 phases to arrive from HBM), loads the
+// record of tile q+2NS-1 into the slot it just freed (NS phases ahead), then runs the visited
+// tests of tile q (hot copy in shared memory, else one L2 probe of the visited|discovered pair)
+// and its RED.ORs.  Slots are compile-time indices of a loop unrolled NS times, so no register
+// ever moves between slots (a moved register would wait for its load).
+#ifndef BFS200_K1PIPE
+#define BFS200_K1PIPE 3
+#endif
+template <int E, bool SEG1, bool POS32, int NS>
+__device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
+                                           uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vd, uint32_t hw,
+                                           uint32_t sa, int bl, uint32_t bmask, int lane) {
+  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
+  Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
+  uint32_t rlen[NS];
+  auto rec_load = [&](int slot, uint32_t t) {
+    rlen[slot] = 0u;
+    rpos[slot] = 0;
+    if (t < nA) {
+      const uint4 r = tileA[t];
+      rpos[slot] = POS32 ? (Pos)r.x : (Pos)((ull)r.x | ((ull)r.y << 32));
+      rlen[slot] = r.z;
+    }
+  };
+  auto rows_issue = [&](int slot) {  // from the record in the same slot
+    const uint32_t* rp = row + rpos[slot] + lane;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      v[slot][e] = 0xFFFFFFFFu;
+      ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);  // Alg.3 line 4
+    }
+  };
+  // prologue: rows of tiles 0 .. NS-2 issued; records of tiles NS-1 .. 2NS-2 prefetched
+  // (the warp's tile q is t0 + q*stride; tile ids and counts fit in 32 bits: tileA holds < 2^32)
+#pragma unroll
+  for (int k = 0; k < NS - 1; ++k) {
+    rec_load(k, t0 + (uint32_t)k * stride);
+    rows_issue(k);
+  }
+#pragma unroll
+  for (int k = 0; k < NS - 1; ++k) rec_load(k, t0 + (uint32_t)(NS + k) * stride);
+  rec_load(NS - 1, t0 + (uint32_t)(NS - 1) * stride);
+  const uint32_t ahead = (uint32_t)(2 * NS - 1) * stride;
+  for (uint32_t t = t0;;) {
+#pragma unroll
+    for (int p = 0; p < NS; ++p) {
+      if (t >= nA) return;  // warp-uniform
+      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (its record is loaded)
+      rows_issue(sn);
+      rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
+      uint32_t x[E], y[E], need[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
+        const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
+        if (SEG1) probe2_seg1(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd);
+        else probe2_segs(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd, bl, bmask);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], y[e], need[e], vd);  // Alg.3 line 7
+      t += stride;
+    }
+  }
+}
+
 template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
                                             const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
@@ -724,7 +909,10 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
       }
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
-    {
+    if constexpr (!P1 && BFS200_K1PIPE > 0 && E <= 8) {
+      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE>(row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vd, hw, sa,
+                                                    bl, bmask, lane);
+    } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;
     uint4 rec1 = t1 < nA ? tileA[t1] : make_uint4(0, 0, 0, 0);

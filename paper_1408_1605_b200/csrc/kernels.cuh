@@ -18,7 +18,6 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, bool force_pos64,
                           cudaStream_t s);
 uint32_t expand_tile_edges(int edges_per_thread);
-size_t seg_scan_tmp_bytes(uint64_t nseg);
 
 // K4: parent claim for the rows discovered in this level (+ pack of the fold message, C > 1).
 cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s);
