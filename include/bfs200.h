@@ -44,7 +44,8 @@ typedef enum {
   BFS_ENOMEM = -3, /* device or host allocation failed                                       */
   BFS_ECUDA = -4,  /* CUDA runtime error (graph becomes unusable)                            */
   BFS_ENCCL = -5,  /* NCCL error (graph becomes unusable)                                    */
-  BFS_ESTATE = -6  /* graph unusable after an earlier fatal error, or call out of order      */
+  BFS_ESTATE = -6, /* graph unusable after an earlier fatal error, or call out of order      */
+  BFS_EPARSE = -7  /* edge-list file does not parse (bfs_load_edges; the detail names the line) */
 } bfs_status;
 
 typedef struct bfs_graph bfs_graph; /* opaque; owned by the library until bfs_destroy */
@@ -204,6 +205,21 @@ int bfs_gather(bfs_graph* g, const int64_t* parent, const int32_t* level, int64_
 
 /* NULL-safe, idempotent for NULL.  Collective with NCCL. */
 void bfs_destroy(bfs_graph* g);
+
+/* Edge-list files (the paper's real-world graphs from the Stanford Large
+ * Network Dataset Collection), for bfs_graph_create:
+ *   BFS_FMT_SNAP_TEXT    lines of two whitespace-separated decimal ids (extra fields ignored);
+ *                        lines starting with '#' or '%' and blank lines are skipped;
+ *   BFS_FMT_BINARY_PAIRS consecutive 16-byte records of two little-endian u64 ids.
+ * Host only (no GPU).  On success *src / *dst are malloc'ed arrays of *nedges tuples in file
+ * order (duplicates and self-loops kept: they count for m_comp) owned by the caller (release with
+ * bfs_free_edges), and *nverts = max id + 1 (0 for an empty file; bfs_graph_create pads it).
+ * Errors (nothing allocated, outputs zeroed): BFS_EINVAL (null argument, unknown format, file
+ * cannot be opened), BFS_EPARSE (malformed line -- bfs_last_error names file:line -- or a binary
+ * file whose size is not a multiple of 16), BFS_ERANGE (an id >= 2^48), BFS_ENOMEM. */
+enum { BFS_FMT_SNAP_TEXT = 0, BFS_FMT_BINARY_PAIRS = 1 };
+int bfs_load_edges(const char* path, int format, uint64_t** src, uint64_t** dst, uint64_t* nedges, uint64_t* nverts);
+void bfs_free_edges(uint64_t* src, uint64_t* dst);
 
 const char* bfs_strerror(int status);
 const char* bfs_last_error(void);

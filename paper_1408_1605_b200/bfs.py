@@ -17,7 +17,8 @@ from . import _build
 
 _LIB = os.environ.get("BFS200_LIB") or _build.LIB  # BFS200_LIB: an alternative build of the same ABI (A/B runs)
 
-BFS_OK, BFS_EINVAL, BFS_ERANGE, BFS_ENOMEM, BFS_ECUDA, BFS_ENCCL, BFS_ESTATE = 0, -1, -2, -3, -4, -5, -6
+BFS_OK, BFS_EINVAL, BFS_ERANGE, BFS_ENOMEM, BFS_ECUDA, BFS_ENCCL, BFS_ESTATE, BFS_EPARSE = 0, -1, -2, -3, -4, -5, -6, -7
+FMT = {"snap-text": 0, "binary-pairs": 1}
 
 
 class BfsError(RuntimeError):
@@ -58,7 +59,8 @@ class LevelRecord(ctypes.Structure):
 
 
 EXPORTS = ["bfs_nccl_unique_id", "bfs_graph_create", "bfs_graph_info", "bfs_set_opts", "bfs_degree", "bfs_run",
-           "bfs_mcomp", "bfs_level_times", "bfs_gather", "bfs_destroy", "bfs_strerror", "bfs_last_error"]
+           "bfs_mcomp", "bfs_level_times", "bfs_gather", "bfs_load_edges", "bfs_free_edges", "bfs_destroy",
+           "bfs_strerror", "bfs_last_error"]
 DEBUG_POS64 = 1
 
 _lib = None
@@ -84,14 +86,20 @@ def lib(build: bool = False):
         L.bfs_mcomp.argtypes = [p, ctypes.POINTER(u64)]
         L.bfs_level_times.argtypes = [p, ctypes.POINTER(LevelRecord), i, ctypes.POINTER(i)]
         L.bfs_gather.argtypes = [p, p, p, p, p]
+        pu64 = ctypes.POINTER(ctypes.c_uint64)
+        L.bfs_load_edges.argtypes = [ctypes.c_char_p, i, ctypes.POINTER(pu64), ctypes.POINTER(pu64),
+                                     ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.bfs_free_edges.argtypes = [pu64, pu64]
+        L.bfs_free_edges.restype = None
         L.bfs_destroy.argtypes = [p]
         L.bfs_destroy.restype = None
         L.bfs_strerror.argtypes = [i]
         L.bfs_strerror.restype = ctypes.c_char_p
         L.bfs_last_error.argtypes = []
         L.bfs_last_error.restype = ctypes.c_char_p
-        for name in EXPORTS[:-3]:
-            getattr(L, name).restype = ctypes.c_int
+        for name in EXPORTS:
+            if name not in ("bfs_destroy", "bfs_free_edges", "bfs_strerror", "bfs_last_error"):
+                getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -115,6 +123,24 @@ def _ptr(x):
             raise ValueError("tensor must be contiguous")
         return x.data_ptr()
     raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def load_edges(path: str, fmt: str = "snap-text"):
+    """bfs_load_edges: (src uint64[m], dst uint64[m], nverts) of a SNAP text / binary-pairs file
+    (host numpy arrays, copied out of the library's buffers)."""
+    L = lib()
+    pu64 = ctypes.POINTER(ctypes.c_uint64)
+    s, d = pu64(), pu64()
+    m, nv = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(L.bfs_load_edges(os.fsencode(path), FMT[fmt] if isinstance(fmt, str) else int(fmt), ctypes.byref(s),
+                            ctypes.byref(d), ctypes.byref(m), ctypes.byref(nv)))
+    try:
+        n = int(m.value)
+        src = np.ctypeslib.as_array(s, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+        dst = np.ctypeslib.as_array(d, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+    finally:
+        L.bfs_free_edges(s, d)
+    return src.astype(np.uint64, copy=False), dst.astype(np.uint64, copy=False), int(nv.value)
 
 
 def nccl_unique_id() -> bytes:

@@ -102,7 +102,7 @@ struct Rank {
   uint32_t* tile_k = nullptr;            // [nnz/32 + 2] first frontier index of every expansion tile
   uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
   void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
-  void* seg_off = nullptr;               // [nseg+1] their exclusive scan (seg_off[nseg] = level total)
+  void* seg_off = nullptr;               // [nseg+1] K3 scratch: per-CTA totals of the count pass and their scan
   uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution

@@ -196,7 +196,7 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.tileA, (3 * (rk.nnz / 32) + 64) * 16);    // long tiles: <= nnz/TILE + #long columns (d >= TILE/2)
   AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
   AL(rk.seg_tot, (nseg + 1) * 32);
-  AL(rk.seg_off, (nseg + 1) * 32);
+  AL(rk.seg_off, (nseg + 8) * 32);  // CTA totals (nseg/8 + 1) and their scan (nseg/8 + 2)
   CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
@@ -1226,6 +1226,7 @@ const char* bfs_strerror(int status) {
     case BFS_ECUDA: return "CUDA error";
     case BFS_ENCCL: return "NCCL error";
     case BFS_ESTATE: return "graph in unusable state";
+    case BFS_EPARSE: return "edge-list parse error";
     default: return "unknown status";
   }
 }

@@ -128,12 +128,9 @@ struct SegTot {
 static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
 // Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
 // chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
-__global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
-                                                              uint64_t nseg, const ull* __restrict__ col,
-                                                              SegTot* seg_tot, int tile_shift) {
+__device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uint64_t nwords, uint64_t seg,
+                                            const ull* __restrict__ col, int tile_shift) {
   const int lane = threadIdx.x & 31;
-  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
-  if (seg >= nseg) return;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
@@ -145,10 +142,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
       const uint64_t w = w0 + 32 * c + lane;
       any |= (w < w1) ? __ldg(bm + w) : 0u;
     }
-    if (!__any_sync(0xFFFFFFFFu, any != 0u)) {
-      if (lane == 0) seg_tot[seg] = SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
-      return;
-    }
+    if (!__any_sync(0xFFFFFFFFu, any != 0u)) return SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
   }
   __shared__ uint16_t s_lists[kScanThreads / 32][1024];
   uint16_t* s_list = s_lists[threadIdx.x >> 5];
@@ -215,7 +209,31 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
     t.ss += __shfl_xor_sync(0xFFFFFFFFu, t.ss, o);
     t.ls += __shfl_xor_sync(0xFFFFFFFFu, t.ls, o);
   }
-  if (lane == 0) seg_tot[seg] = t;
+  return t;
+}
+
+// Per-segment totals (seg_tot[seg]) and per-CTA totals of the kScanThreads/32 segments of a CTA
+// (cta_tot[b]): the single-CTA scan (k_seg_scan) then only scans the few CTA totals, and the
+// emit pass adds the in-CTA prefix itself.
+__global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
+                                                              uint64_t nseg, const ull* __restrict__ col,
+                                                              SegTot* seg_tot, SegTot* cta_tot, int tile_shift) {
+  __shared__ SegTot s_t[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
+  const SegTot t = seg < nseg ? count_seg(bm, nwords, seg, col, tile_shift) : SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
+  if (lane == 0) {
+    if (seg < nseg) seg_tot[seg] = t;
+    s_t[wid] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SegTot c{0u, 0u, 0u, 0u, 0ull, 0ull};
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w)
+      c = SegTot{c.cs + s_t[w].cs, c.na + s_t[w].na, c.nh + s_t[w].nh, 0u, c.ss + s_t[w].ss, c.ls + s_t[w].ls};
+    cta_tot[blockIdx.x] = c;
+  }
 }
 
 #ifndef BFS200_BLIND3
@@ -228,9 +246,10 @@ constexpr bool kBlind3 = BFS200_BLIND3;
 constexpr ull kP2Factor = 8;
 constexpr ull kM3Factor = 4;
 
-// K3 scan of the per-segment totals, one CTA (the totals are few: one per 4096 columns), fused
-// with the level bookkeeping: seg_off[k] = exclusive scan of seg_tot (seg_off[nseg] = the level's
-// totals), then the per-level counters and the parent-claim mode.  Pass k scans segments
+// K3 scan of the per-CTA totals of the count pass, one CTA (the totals are few: one per 32 K
+// columns), fused with the level bookkeeping: seg_off[k] = exclusive scan of seg_tot[0..nseg)
+// (here: the CTA totals; seg_off[nseg] = the level's totals), then the per-level counters and the
+// parent-claim mode.  Pass k scans segments
 // [1024k, 1024k + 1024): warp inclusive scans by shuffles, the 32 warp totals scanned by warp 0
 // through shared memory, a running carry; the next pass's totals are loaded during this one.
 constexpr int kSegScanThreads = 1024;
@@ -329,18 +348,23 @@ __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __re
 // lane b handles bit b (coalesced col reads and list writes), col loads of 4 words in flight.
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                              uint64_t nseg, const ull* __restrict__ col,
-                                                             const SegTot* seg_off, uint32_t* flist, ull* rowoff,
+                                                             const SegTot* seg_tot, const SegTot* cta_off,
+                                                             uint32_t* flist, ull* rowoff,
                                                              ull* cumul, uint32_t* tile_k, uint4* tileA,
                                                              int tile_shift, uint4* longlist, LevelInfo* info) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
   if (seg >= nseg) return;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
-  const SegTot o = seg_off[seg];
+  SegTot o = cta_off[blockIdx.x];  // + the totals of this CTA's earlier segments
+  for (int w2 = 0; w2 < wid; ++w2) {
+    const SegTot q = seg_tot[(uint64_t)blockIdx.x * (kScanThreads / 32) + w2];
+    o = SegTot{o.cs + q.cs, o.na + q.na, o.nh + q.nh, 0u, o.ss + q.ss, o.ls + q.ls};
+  }
   {  // nothing to emit (no column of non-zero degree in the segment): skip the bitmap
-    const SegTot o1 = seg_off[seg + 1];
-    if (o1.cs == o.cs && o1.na == o.na) return;
+    const SegTot mine = seg_tot[seg];
+    if (mine.cs == 0 && mine.na == 0) return;
   }
   uint64_t k = o.cs;  // next short list position
   ull e = o.ss;       // next short edge position
@@ -530,12 +554,13 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   const unsigned grid = (unsigned)((nseg + kScanThreads / 32 - 1) / (kScanThreads / 32));
   const int ts = __builtin_ctz(tile_edges);
   SegTot* st = static_cast<SegTot*>(rk.seg_tot);
-  SegTot* so = static_cast<SegTot*>(rk.seg_off);
-  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ts);
-  // exclusive scan of the nseg segment totals (so[nseg] = level total) + the level's counters
-  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(st, nseg, so, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
+  SegTot* ct = static_cast<SegTot*>(rk.seg_off);  // [grid] CTA totals, then [grid + 1] their scan
+  SegTot* co = ct + grid;
+  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts);
+  // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
+  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
                                           kM3Factor, (ull)g.nrows());
-  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, so, rk.flist, rk.rowoff,
+  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff,
                                             rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
   return cudaGetLastError();
@@ -684,90 +709,84 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
   }
 }
 
-// Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
-// keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
-// word address from v (two instructions instead of three live registers per row).
-__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
-                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd) {
+// Long-column tiles of a P2 level, software-pipelined (the hot loop of the peak level).  A warp
+// walks its tiles q = 0, 1, ... (tile id t0 + q*stride) through NS row slots.  Phase q: the
+// `row` loads of tile q+NS-1 (into the slot tile q-1 freed), the record of tile q+2NS-1 (NS
+// phases ahead), then the visited tests of tile q -- hot copy in shared memory, else one L2 probe
+// of the visited|discovered pair -- and its RED.ORs (Alg.3 lines 4-7).  So every tile's rows have
+// NS-1 phases to arrive from HBM and no phase waits for a record.  Slots are compile-time indices
+// of a loop unrolled NS times (no register moves between slots: a moved register waits for its
+// load).  A row id of 0xFFFFFFFF marks a lane past the tile's end (partial last tile of a column,
+// or past the warp's last tile); a probe that is not needed returns x = 0xFFFFFFFF (no RED).
+// (Measured at s26, peak level: rows 1 / 2 / 3 tiles ahead 3.20 / 3.08 / 4.24 ms (3 spills);
+// REDs deferred by one phase behind the next tile's probes: 3.34 ms (rows 1 ahead) / 4.11 ms.)
+#ifndef BFS200_K1PIPE
+#define BFS200_K1PIPE 3
+#endif
+__device__ __forceinline__ void probe3(uint32_t& x, uint32_t& y, uint32_t v, uint32_t hw, uint32_t sa,
+                                       const uint32_t* vd) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, m;\n"
       " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %4, %5;\n"
-      " shr.b32 wi, %3, 5;\n"
-      " min.u32 hi, wi, %6;\n"
+      " setp.ne.u32 pok, %2, -1;\n"
+      " shr.b32 wi, %2, 5;\n"
+      " min.u32 hi, wi, %3;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %7;\n"
+      " add.u32 hi, hi, %4;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " shf.l.wrap.b32 m, 0, 1, %2;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %8;\n"
+      " mad.wide.u32 a, wi, 8, %5;\n"
+      " mov.b32 %0, -1;\n"
       " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
+      : "=r"(x), "=r"(y)
+      : "r"(v), "r"(hw), "r"(sa), "l"(vd));
 }
-__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
-                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd, int bl,
-                                            uint32_t bmask) {
+__device__ __forceinline__ void probe3_segs(uint32_t& x, uint32_t& y, uint32_t v, uint32_t hw, uint32_t sa,
+                                            const uint32_t* vd, int bl, uint32_t bmask) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, sg, off, m;\n"
       " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %4, %5;\n"
-      " shr.b32 wi, %3, 5;\n"
-      " shr.b32 sg, %3, %9;\n"
-      " and.b32 off, %3, %10;\n"
+      " setp.ne.u32 pok, %2, -1;\n"
+      " shr.b32 wi, %2, 5;\n"
+      " shr.b32 sg, %2, %6;\n"
+      " and.b32 off, %2, %7;\n"
       " shr.b32 off, off, 5;\n"
-      " min.u32 off, off, %6;\n"
-      " add.u32 hv, %6, 1;\n"
+      " min.u32 off, off, %3;\n"
+      " add.u32 hv, %3, 1;\n"
       " mad.lo.u32 hi, sg, hv, off;\n"
-      " selp.u32 hi, hi, %6, pok;\n"
+      " selp.u32 hi, hi, %3, pok;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %7;\n"
+      " add.u32 hi, hi, %4;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " shf.l.wrap.b32 m, 0, 1, %2;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %8;\n"
+      " mad.wide.u32 a, wi, 8, %5;\n"
+      " mov.b32 %0, -1;\n"
       " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+      : "=r"(x), "=r"(y)
+      : "r"(v), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
 }
-__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
-  asm volatile("{\n"
-               " .reg .pred pn, pr;\n"
-               " .reg .b32 t, m, wi;\n"
-               " .reg .b64 a;\n"
-               " setp.ne.b32 pn, %3, 0;\n"
-               " shf.l.wrap.b32 m, 0, 1, %0;\n"
-               " lop3.b32 t, %1, %2, m, 0xa8;\n"
-               " setp.eq.and.b32 pr, t, 0, pn;\n"
-               " shr.b32 wi, %0, 5;\n"
-               " mad.wide.u32 a, wi, 8, %4;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
-               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
+// RED.OR of v's discovered bit unless the probe found it visited or discovered (or was not needed).
+// (Written in C++ around red_or_if: the equivalent single asm block with its own setp makes
+// ptxas 12.9 crash on this loop.)
+__device__ __forceinline__ void red3(uint32_t v, uint32_t x, uint32_t y, uint32_t* vd) {
+  const uint32_t m = 1u << (v & 31);
+  red_or_if(((x | y) & m) == 0u, vd + 2 * (v >> 5) + 1, m);
 }
 
-// Long-column tiles of a P2 level, software-pipelined (the hot loop of the peak level).  A warp
-// walks its tiles q = 0, 1, ... (tile id t0 + q*stride) through NS slots: in phase q it issues the
-// `row` loads of tile q+NS-1 (so every tile's rows have NS-1 phases to arrive from HBM), loads the
-// record of tile q+2NS-1 into the slot it just freed (NS phases ahead), then runs the visited
-// tests of tile q (hot copy in shared memory, else one L2 probe of the visited|discovered pair)
-// and its RED.ORs.  Slots are compile-time indices of a loop unrolled NS times, so no register
-// ever moves between slots (a moved register would wait for its load).
-#ifndef BFS200_K1PIPE
-#define BFS200_K1PIPE 3
-#endif
 template <int E, bool SEG1, bool POS32, int NS>
 __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
                                            uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vd, uint32_t hw,
                                            uint32_t sa, int bl, uint32_t bmask, int lane) {
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  constexpr uint32_t TILE = 32u * E;
   uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
   Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
   uint32_t rlen[NS];
@@ -782,14 +801,19 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
   };
   auto rows_issue = [&](int slot) {  // from the record in the same slot
     const uint32_t* rp = row + rpos[slot] + lane;
+    if (rlen[slot] == TILE) {  // full tile (warp-uniform): no per-lane bounds
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      v[slot][e] = 0xFFFFFFFFu;
-      ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);  // Alg.3 line 4
+      for (int e = 0; e < E; ++e) v[slot][e] = ld_stream_u32(rp + 32 * e);  // Alg.3 line 4
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        v[slot][e] = 0xFFFFFFFFu;
+        ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);
+      }
     }
   };
   // prologue: rows of tiles 0 .. NS-2 issued; records of tiles NS-1 .. 2NS-2 prefetched
-  // (the warp's tile q is t0 + q*stride; tile ids and counts fit in 32 bits: tileA holds < 2^32)
+  // (the warp's tile q is t0 + q*stride; ids stay below 2^32: t < nA + 2*NS*stride)
 #pragma unroll
   for (int k = 0; k < NS - 1; ++k) {
     rec_load(k, t0 + (uint32_t)k * stride);
@@ -803,18 +827,17 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
 #pragma unroll
     for (int p = 0; p < NS; ++p) {
       if (t >= nA) return;  // warp-uniform
-      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (its record is loaded)
+      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (= of tile q-1, done)
       rows_issue(sn);
-      rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
-      uint32_t x[E], y[E], need[E];
+      rec_load(sn, t + ahead);
+      uint32_t x[E], y[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
-        const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
-        if (SEG1) probe2_seg1(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd);
-        else probe2_segs(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd, bl, bmask);
+      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
+        if (SEG1) probe3(x[e], y[e], v[p][e], hw, sa, vd);
+        else probe3_segs(x[e], y[e], v[p][e], hw, sa, vd, bl, bmask);
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], y[e], need[e], vd);  // Alg.3 line 7
+      for (int e = 0; e < E; ++e) red3(v[p][e], x[e], y[e], vd);  // Alg.3 line 7
       t += stride;
     }
   }

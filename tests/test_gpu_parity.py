@@ -337,6 +337,45 @@ def test_gather_loopback(bfs):
     assert np.array_equal(la, lv) and np.array_equal(pad.cpu().numpy(), pa)
 
 
+# ---------------------------------------------------------------- real-world graph files (NEXT-4)
+SNAP_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "snap_small.txt")
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 2), (1, 3)])
+def test_snap_file_parity(bfs, grid):
+    """A SNAP-format file (tests/golden/snap_small.txt: sparse ids, duplicates, self-loops, two
+    components) through bfs_load_edges -> bfs_graph_create (nverts = max id + 1, padded): every
+    vertex of the file as root, bit-exact against the oracle on the same tuples."""
+    src, dst, n = bfs.load_edges(SNAP_GOLDEN)
+    og = oracle.Graph(n, src, dst)
+    g = make_graph(bfs, src, dst, n, *grid, on_device=False)
+    for r in np.unique(np.concatenate([src, dst])).tolist() + [0, n - 1]:
+        check_root(g, og, int(r), n)
+
+
+def test_snap_kronecker_roundtrip(bfs, tmp_path):
+    """The s14 Kronecker tuples written as a SNAP text file and as binary pairs, loaded back and
+    searched: identical to the oracle on the generator's own tuples."""
+    scale = 14
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    txt = tmp_path / "kron.txt"
+    with open(txt, "w") as f:
+        f.write("# Directed graph: kron s14\n# FromNodeId\tToNodeId\n")
+        f.write("".join(f"{a}\t{b}\n" for a, b in zip(s.tolist(), d.tolist())))
+    binp = tmp_path / "kron.bin"
+    binp.write_bytes(np.stack([s, d], 1).astype("<u8").tobytes())
+    roots = inputs.sample_roots(n, 4, inputs.nonisolated_mask(n, s, d))
+    for path, fmt in ((txt, "snap-text"), (binp, "binary-pairs")):
+        ls, ld, nv = bfs.load_edges(str(path), fmt)
+        assert np.array_equal(ls, s) and np.array_equal(ld, d) and nv == int(max(s.max(), d.max())) + 1
+        og = oracle.Graph(nv, s, d)
+        g = make_graph(bfs, ls, ld, nv, 2, 2)
+        for r in roots:
+            check_root(g, og, r, nv)
+        g.close()
+
+
 # ---------------------------------------------------------------- full size (bench config)
 def test_s26_bench_config_graph500_valid(bfs):
     """s26 1x1 (configs[2], the bench workload): device-generated graph, bench launch options,
