@@ -717,68 +717,83 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 // NS-1 phases to arrive from HBM and no phase waits for a record.  Slots are compile-time indices
 // of a loop unrolled NS times (no register moves between slots: a moved register waits for its
 // load).  A row id of 0xFFFFFFFF marks a lane past the tile's end (partial last tile of a column,
-// or past the warp's last tile); a probe that is not needed returns x = 0xFFFFFFFF (no RED).
-// (Measured at s26, peak level: rows 1 / 2 / 3 tiles ahead 3.20 / 3.08 / 4.24 ms (3 spills);
-// REDs deferred by one phase behind the next tile's probes: 3.34 ms (rows 1 ahead) / 4.11 ms.)
+// or past the warp's last tile).  Not inlined: its registers are allocated apart from the rest of
+// k_expand (inlined, the short-tile state live across it made both spill).
+// Measured at s26, peak level (tools/ab_expand.py, same box, two runs each): the previous
+// double-buffered loop 3.19 ms; this loop with NS = 2 / 3 / 4: 3.20 / 3.08 / 4.24 ms (NS = 4
+// spills); the REDs deferred one phase behind the next tile's probes: 3.34 ms (NS = 2); a
+// warp-uniform full-tile branch without per-lane bounds: 3.46 ms; a probe returning x = ~0 instead
+// of a need flag: 3.17 ms.
 #ifndef BFS200_K1PIPE
 #define BFS200_K1PIPE 3
 #endif
-__device__ __forceinline__ void probe3(uint32_t& x, uint32_t& y, uint32_t v, uint32_t hw, uint32_t sa,
-                                       const uint32_t* vd) {
+// Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
+// keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
+// word address from v (two instructions instead of three live registers per row).
+__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
+                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, m;\n"
       " .reg .b64 a;\n"
-      " setp.ne.u32 pok, %2, -1;\n"
-      " shr.b32 wi, %2, 5;\n"
-      " min.u32 hi, wi, %3;\n"
+      " setp.lt.u32 pok, %4, %5;\n"
+      " shr.b32 wi, %3, 5;\n"
+      " min.u32 hi, wi, %6;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %4;\n"
+      " add.u32 hi, hi, %7;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %2;\n"
+      " shf.l.wrap.b32 m, 0, 1, %3;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %5;\n"
-      " mov.b32 %0, -1;\n"
+      " mad.wide.u32 a, wi, 8, %8;\n"
       " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y)
-      : "r"(v), "r"(hw), "r"(sa), "l"(vd));
+      : "=r"(x), "=r"(y), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
 }
-__device__ __forceinline__ void probe3_segs(uint32_t& x, uint32_t& y, uint32_t v, uint32_t hw, uint32_t sa,
-                                            const uint32_t* vd, int bl, uint32_t bmask) {
+__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
+                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd, int bl,
+                                            uint32_t bmask) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, sg, off, m;\n"
       " .reg .b64 a;\n"
-      " setp.ne.u32 pok, %2, -1;\n"
-      " shr.b32 wi, %2, 5;\n"
-      " shr.b32 sg, %2, %6;\n"
-      " and.b32 off, %2, %7;\n"
+      " setp.lt.u32 pok, %4, %5;\n"
+      " shr.b32 wi, %3, 5;\n"
+      " shr.b32 sg, %3, %9;\n"
+      " and.b32 off, %3, %10;\n"
       " shr.b32 off, off, 5;\n"
-      " min.u32 off, off, %3;\n"
-      " add.u32 hv, %3, 1;\n"
+      " min.u32 off, off, %6;\n"
+      " add.u32 hv, %6, 1;\n"
       " mad.lo.u32 hi, sg, hv, off;\n"
-      " selp.u32 hi, hi, %3, pok;\n"
+      " selp.u32 hi, hi, %6, pok;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %4;\n"
+      " add.u32 hi, hi, %7;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %2;\n"
+      " shf.l.wrap.b32 m, 0, 1, %3;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %5;\n"
-      " mov.b32 %0, -1;\n"
+      " mad.wide.u32 a, wi, 8, %8;\n"
       " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
+      " selp.u32 %2, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y)
-      : "r"(v), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+      : "=r"(x), "=r"(y), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
 }
-// RED.OR of v's discovered bit unless the probe found it visited or discovered (or was not needed).
-// (Written in C++ around red_or_if: the equivalent single asm block with its own setp makes
-// ptxas 12.9 crash on this loop.)
-__device__ __forceinline__ void red3(uint32_t v, uint32_t x, uint32_t y, uint32_t* vd) {
-  const uint32_t m = 1u << (v & 31);
-  red_or_if(((x | y) & m) == 0u, vd + 2 * (v >> 5) + 1, m);
+__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
+  asm volatile("{\n"
+               " .reg .pred pn, pr;\n"
+               " .reg .b32 t, m, wi;\n"
+               " .reg .b64 a;\n"
+               " setp.ne.b32 pn, %3, 0;\n"
+               " shf.l.wrap.b32 m, 0, 1, %0;\n"
+               " lop3.b32 t, %1, %2, m, 0xa8;\n"
+               " setp.eq.and.b32 pr, t, 0, pn;\n"
+               " shr.b32 wi, %0, 5;\n"
+               " mad.wide.u32 a, wi, 8, %4;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
+               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
 }
 
 template <int E, bool SEG1, bool POS32, int NS>
@@ -786,7 +801,6 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
                                            uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vd, uint32_t hw,
                                            uint32_t sa, int bl, uint32_t bmask, int lane) {
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
-  constexpr uint32_t TILE = 32u * E;
   uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
   Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
   uint32_t rlen[NS];
@@ -801,19 +815,14 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
   };
   auto rows_issue = [&](int slot) {  // from the record in the same slot
     const uint32_t* rp = row + rpos[slot] + lane;
-    if (rlen[slot] == TILE) {  // full tile (warp-uniform): no per-lane bounds
 #pragma unroll
-      for (int e = 0; e < E; ++e) v[slot][e] = ld_stream_u32(rp + 32 * e);  // Alg.3 line 4
-    } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        v[slot][e] = 0xFFFFFFFFu;
-        ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);
-      }
+    for (int e = 0; e < E; ++e) {
+      v[slot][e] = 0xFFFFFFFFu;
+      ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);  // Alg.3 line 4
     }
   };
   // prologue: rows of tiles 0 .. NS-2 issued; records of tiles NS-1 .. 2NS-2 prefetched
-  // (the warp's tile q is t0 + q*stride; ids stay below 2^32: t < nA + 2*NS*stride)
+  // (the warp's tile q is t0 + q*stride; tile ids and counts fit in 32 bits: tileA holds < 2^32)
 #pragma unroll
   for (int k = 0; k < NS - 1; ++k) {
     rec_load(k, t0 + (uint32_t)k * stride);
@@ -827,21 +836,23 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
 #pragma unroll
     for (int p = 0; p < NS; ++p) {
       if (t >= nA) return;  // warp-uniform
-      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (= of tile q-1, done)
+      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (its record is loaded)
       rows_issue(sn);
-      rec_load(sn, t + ahead);
-      uint32_t x[E], y[E];
+      rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
+      uint32_t x[E], y[E], need[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
-        if (SEG1) probe3(x[e], y[e], v[p][e], hw, sa, vd);
-        else probe3_segs(x[e], y[e], v[p][e], hw, sa, vd, bl, bmask);
+      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
+        const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
+        if (SEG1) probe2_seg1(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd);
+        else probe2_segs(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd, bl, bmask);
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) red3(v[p][e], x[e], y[e], vd);  // Alg.3 line 7
+      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], y[e], need[e], vd);  // Alg.3 line 7
       t += stride;
     }
   }
 }
+
 
 template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
