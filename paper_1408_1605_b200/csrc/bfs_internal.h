@@ -36,8 +36,10 @@ struct LevelInfo {
   unsigned long long disc_total;  // rows discovered by this rank so far in this search (K4 counts)
   unsigned long long blind;   // mode 3 with few rows visited: claims without the visited probe
                               // for rows past the hot prefix (K4 masks the visited rows)
-  unsigned long long pad[5];
+  // capacities of this rank's arrays, for the bounds checks of a BFS200_CHECKS build (kernels.cu)
+  unsigned long long cap_nnz, cap_ncols, cap_nrows, cap_tiles, cap_long;
 };
+static_assert(sizeof(LevelInfo) == 128, "LevelInfo layout");
 
 // One slot of the peer-exchange signal array (one slot per sending rank).
 struct XSig {

@@ -21,12 +21,21 @@
 #include <new>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.h"
 #include "kernels.cuh"
 
 namespace bfs200 {
 
 typedef unsigned long long ull;
+
+// NVTX ranges (host-side enqueue phases: graph construction, level loop, parent resolution,
+// outputs) for Nsight timelines; no cost when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // head of LevelCtrl read by the host each level (everything before the per-level arrays)
 constexpr size_t kCtrlHead = offsetof(LevelCtrl, lvl_frontier);
@@ -201,6 +210,11 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
   AL(rk.scratch, 64 * 8);
+  {  // array capacities for the bounds checks of a BFS200_CHECKS build (kernels.cu)
+    const unsigned long long caps[5] = {rk.nnz, g.ncols(), g.nrows(), 3 * (rk.nnz / 32) + 64,
+                                        2 * (rk.nnz / 256 + 64)};
+    CKR(cudaMemcpyAsync(&rk.info->cap_nnz, caps, sizeof caps, cudaMemcpyHostToDevice, G.stream));
+  }
   if (g.C > 1) {
     AL(rk.sendbuf, rw * 4);
     AL(rk.recv, (uint64_t)g.C * W * 4);
@@ -883,6 +897,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
       G.broken = false;
     }
   }
+  NvtxRange r_loop(use_graph ? "bfs200: level loop (CUDA graph)" : "bfs200: level loop (host-driven)");
   if (use_graph) {
     CKR(cudaGraphLaunch(G.gexec, s));
   } else {
@@ -918,6 +933,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     CKR(cudaEventRecord(G.tail_ev[0], s));
   }
   if (g.C > 1 && parent) {
+    NvtxRange r_res("bfs200: parent resolution");
     if ((rc = resolve_parents(G))) return rc;
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
@@ -1029,6 +1045,7 @@ int bfs_graph_create(const uint64_t* src, const uint64_t* dst, uint64_t nedges, 
     return set_err(BFS_ENOMEM, "host allocation failed");
   }
   try {
+    NvtxRange r_create("bfs200: bfs_graph_create");
     rc = create(src, dst, nedges, nverts, R, C, comm, opts, &gp->G);
   } catch (std::bad_alloc&) {
     rc = set_err(BFS_ENOMEM, "host allocation failed");
@@ -1104,6 +1121,7 @@ int bfs_degree(bfs_graph* gp, uint64_t v, uint64_t* degree) {
 
 int bfs_run(bfs_graph* gp, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
   ENTER(gp);
+  NvtxRange r_run("bfs200: bfs_run");
   if (root >= G.g.nverts) return set_err(BFS_ERANGE, "root %llu >= nverts %llu", (ull)root, (ull)G.g.nverts);
   try {
     return run(G, root, parent, level, stats);

@@ -72,6 +72,23 @@ __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
                ::"l"(a), "r"(m), "r"((int)p));
 }
 
+// Bounds checks (a BFS200_CHECKS=1 build; compute-sanitizer is not available on the GPU pool):
+// an index outside its array traps the kernel, which the caller sees as BFS_ECUDA.  Capacities
+// come from LevelInfo (set by alloc_state).  Off in production builds.
+#ifndef BFS200_CHECKS
+#define BFS200_CHECKS 0
+#endif
+#if BFS200_CHECKS
+#define BCHECK(c)     \
+  do {                \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define BCHECK(c) \
+  do {            \
+  } while (0)
+#endif
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -380,9 +397,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
       for (unsigned q = 0; q < nt; ++q) {
         const ull pos = c0 + ((ull)q << tile_shift);
         const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+        BCHECK(pa + q < info->cap_tiles && pos + len <= info->cap_nnz);
         tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
       }
     } else {  // hub column: its tiles are written by k_tile_fill
+      BCHECK(2 * hub + 1 < info->cap_long && c0 + d <= info->cap_nnz);
       longlist[2 * hub] = make_uint4((uint32_t)pa, nt, (uint32_t)u, (uint32_t)(pa >> 32));
       longlist[2 * hub + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
     }
@@ -438,10 +457,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
           if (ds) {
             const uint64_t pos = k + __popc(smask & lt);
             const ull eb = e + inc - ds;
+            BCHECK(pos < info->cap_ncols && u < info->cap_ncols && c0 + ds <= info->cap_nnz);
             flist[pos] = (uint32_t)u;
             rowoff[pos] = c0;
             cumul[pos] = eb;
-            for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) tile_k[t] = (uint32_t)pos;
+            for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) {
+              BCHECK(t < info->cap_nnz / 32 + 2);
+              tile_k[t] = (uint32_t)pos;
+            }
           }
           if (isl) {
             emit_long(u, c0, d, a + ia - na, na, h + __popc(hmask & lt));
@@ -513,10 +536,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         hh += nt > 8 ? 1u : 0u;
         ++nlongcols;
       } else if (d) {
+        BCHECK(kk < info->cap_ncols && u < info->cap_ncols && c0 + d <= info->cap_nnz);
         flist[kk] = (uint32_t)u;
         rowoff[kk] = c0;
         cumul[kk] = ee;
-        for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) tile_k[t] = (uint32_t)kk;
+        for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) {
+          BCHECK(t < info->cap_nnz / 32 + 2);
+          tile_k[t] = (uint32_t)kk;
+        }
         ++kk;
         ee += d;
       }
@@ -543,6 +570,7 @@ __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4*
     for (uint32_t q = lane; q < h.y; q += 32) {
       const ull pos = c0 + ((ull)q << tile_shift);
       const ull len = min(d - ((ull)q << tile_shift), tm + 1);
+      BCHECK(pa + q < info->cap_tiles && pos + len <= info->cap_nnz);
       tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, h.z);
     }
   }
@@ -799,7 +827,7 @@ __device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t y, uint32_
 template <int E, bool SEG1, bool POS32, int NS>
 __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
                                            uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vd, uint32_t hw,
-                                           uint32_t sa, int bl, uint32_t bmask, int lane) {
+                                           uint32_t sa, int bl, uint32_t bmask, int lane, const LevelInfo* info) {
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
   uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
   Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
@@ -809,6 +837,7 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
     rpos[slot] = 0;
     if (t < nA) {
       const uint4 r = tileA[t];
+      BCHECK(((ull)r.x | ((ull)r.y << 32)) + r.z <= info->cap_nnz && r.z <= 32u * E);
       rpos[slot] = POS32 ? (Pos)r.x : (Pos)((ull)r.x | ((ull)r.y << 32));
       rlen[slot] = r.z;
     }
@@ -841,6 +870,8 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
       rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
       uint32_t x[E], y[E], need[E];
 #pragma unroll
+      for (int e = 0; e < E; ++e) BCHECK(v[p][e] == 0xFFFFFFFFu || v[p][e] < info->cap_nrows);
+#pragma unroll
       for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
         const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
         if (SEG1) probe2_seg1(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd);
@@ -861,8 +892,9 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
                                             ull nA, ull n, ull total, ull all_edges, uint32_t* vd, uint32_t* pmin,
                                             const uint32_t* __restrict__ inv_col, uint32_t hot_words, int C,
                                             uint64_t W, int blog, uint32_t region_words, bool claim3,
-                                            bool blind3) {
+                                            bool blind3, const LevelInfo* info) {
   constexpr int TILE = 32 * E;
+  BCHECK(nA <= info->cap_tiles && total <= info->cap_nnz && n <= info->cap_ncols);
   constexpr int WARPS = THREADS / 32;
   constexpr int SLOT = TILE + 2;
   constexpr int WV = E < 4 ? E : 4;
@@ -945,7 +977,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     ull t = (ull)blockIdx.x * WARPS + wid;
     if constexpr (!P1 && BFS200_K1PIPE > 0 && E <= 8) {
       long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE>(row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vd, hw, sa,
-                                                    bl, bmask, lane);
+                                                    bl, bmask, lane, info);
     } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;
@@ -1003,6 +1035,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   }
   while (tile < ntiles) {
     const ull t0 = tile * TILE;
+    BCHECK(klo <= khi && khi < n);
     const uint32_t len = (uint32_t)min((ull)TILE, total - t0);
     const uint32_t cnt = khi - klo + 1;
     // stage this tile's columns
@@ -1149,10 +1182,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
   if (info->mode != 2)
     expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd,
                                                pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3,
-                                               info->blind != 0);
+                                               info->blind != 0, info);
   else
     expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges,
-                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false, false);
+                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false, false, info);
 }
 
 template <int E, int THREADS>
@@ -1392,6 +1425,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
 #pragma unroll
       for (int i = 0; i < kParRows; ++i) {
         if (r[i] == 0xFFFFFFFFu) continue;
+        BCHECK(r[i] < nwords * 32 && (best[i] == 0xFFFFFFFFu || best[i] < info->cap_ncols));
         if (best[i] != 0xFFFFFFFFu) {
           pred[r[i]] = pv[i];
         } else {  // defer to the whole warp; slot lane+32*nlong <= q0+32i was already read
@@ -1422,6 +1456,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
             break;
           }
         }
+        BCHECK(best < info->cap_ncols);  // a discovered row has a frontier neighbour in its CSR row
         if (lane == 0) pred[r] = inv_col[best];
       }
     }
@@ -1644,6 +1679,7 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t p = pp[k];
+    BCHECK(p < a.block);
     const bool reached = (a.vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
     int64_t v = -1;
     if (reached && parent_out) {  // without a parent output the resolution did not run

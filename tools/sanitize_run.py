@@ -1,9 +1,10 @@
-"""Small BFS workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+"""Small BFS workload for memory-safety runs (the BFS200_CHECKS=1 bounds-checked build through
+BFS200_LIB -- tests/test_gpu_checked.py -- or compute-sanitizer where a pool allows it):
 Kronecker s12 on the 1x1 and 2x2 loopback grids, host-driven and CUDA-graph level loops, every
 K1/K3/K4/K2 path (P1, mode 3, P2 levels; long and short tiles), outputs checked against the
 oracle so a sanitizer-perturbed run is also a parity run.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+    BFS200_LIB=paper_1408_1605_b200/build/variants/libchecked.so SAN_SCALE=18 python tools/sanitize_run.py
 """
 import os
 import sys
