@@ -608,7 +608,10 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
 // parent's global id.
 constexpr ull kHotMinEdges = 1ull << 22;  // stage the hot visited prefix only for big levels
 constexpr size_t kSmemBudget = 227 * 1024;
-constexpr size_t kSmemTarget = 160 * 1024;  // K1 dynamic shared memory (staging + hot copy)
+#ifndef BFS200_SMEM_KB
+#define BFS200_SMEM_KB 160
+#endif
+constexpr size_t kSmemTarget = (size_t)BFS200_SMEM_KB * 1024;  // K1 dynamic shared memory (staging + hot copy)
 // per-warp chunk before the hot-copy region: the warp's short-tile staging (s_off, s_beg)
 template <int E>
 __host__ __device__ constexpr size_t expand_warp_bytes(bool pos32) {
