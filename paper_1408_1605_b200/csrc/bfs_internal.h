@@ -87,10 +87,12 @@ struct Rank {
   uint32_t* inv_own = nullptr;  // [block]
   uint32_t* inv_col = nullptr;  // [ncols]
   // per-search state
-  // visited bitmap over ALL local rows interleaved word by word with the
-  // rows discovered in the current level: vd[2w] = visited word w, vd[2w+1] = discovered word w,
-  // so the expansion tests both with one 8-byte load.
-  uint32_t* vd = nullptr;        // [2 * nrows/32]
+  // visited bitmap over ALL local rows: vis = visited at the level start
+  // OR rows discovered by this rank in the level (the expansion's RED.ORs), so one 4-byte probe
+  // tests "visited or already discovered"; vold = the level-start bits (discovered = vis & ~vold).
+  // Equal between levels.
+  uint32_t* vis = nullptr;       // [nrows/32]
+  uint32_t* vold = nullptr;      // [nrows/32]
   uint32_t* sendbuf = nullptr;   // [nrows/32] discovered rows packed contiguously (fold message, C>1)
   uint32_t* recv = nullptr;      // [C * block/32] fold receive buffer (segment c from P_ic); C>1 only
   uint32_t* all_front = nullptr; // [ncols/32] gathered frontier bitmap; own segment i = own frontier

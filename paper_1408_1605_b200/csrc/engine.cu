@@ -192,7 +192,8 @@ static int alloc_state(Graph& G, Rank& rk) {
 #define AL(ptr, bytes)                                  \
   if ((rc = G_alloc(G, (void**)&(ptr), (bytes))) != 0) \
     return rc;
-  AL(rk.vd, 2 * rw * 4);
+  AL(rk.vis, rw * 4);
+  AL(rk.vold, rw * 4);
   AL(rk.all_front, cw * 4);
   AL(rk.pred, g.nrows() * 4);
   AL(rk.pmin, g.nrows() * 4);

@@ -36,12 +36,6 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   return v;
 }
 
-// visited|discovered pair, cached in L2 only (the discovered word changes during the kernel)
-__device__ __forceinline__ uint2 ld_cg_u2(const uint32_t* p) {
-  uint2 v;
-  asm volatile("ld.global.cg.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t m) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(m) : "memory");
@@ -53,19 +47,15 @@ __device__ __forceinline__ void ld_stream_u32_if(bool p, const uint32_t* a, uint
   asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
                : "+r"(v) : "l"(a), "r"((int)p));
 }
-__device__ __forceinline__ void ld_cg_u2_if(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
-  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
-               : "+r"(x), "+r"(y) : "l"(a), "r"((int)p));
-}
 // predicated loads whose destinations are undefined when the predicate is false (no register
 // initialisation; every use is guarded by the same predicate)
 __device__ __forceinline__ void ld_stream_u32_p(bool p, const uint32_t* a, uint32_t& v) {
   asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.L1::no_allocate.u32 %0, [%1]; }"
       : "=r"(v) : "l"(a), "r"((int)p));
 }
-__device__ __forceinline__ void ld_cg_u2_p(bool p, const uint32_t* a, uint32_t& x, uint32_t& y) {
-  asm("{ .reg .pred q; setp.ne.b32 q, %3, 0; @q ld.global.cg.v2.u32 {%0, %1}, [%2]; }"
-      : "=r"(x), "=r"(y) : "l"(a), "r"((int)p));
+// visited word (L2 only: the bitmap changes during the kernel), undefined when p is false
+__device__ __forceinline__ void ld_cg_u32_p(bool p, const uint32_t* a, uint32_t& x) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cg.u32 %0, [%1]; }" : "=r"(x) : "l"(a), "r"((int)p));
 }
 __device__ __forceinline__ void red_or_if(bool p, uint32_t* a, uint32_t m) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q red.relaxed.gpu.global.or.b32 [%0], %1; }"
@@ -96,11 +86,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // ------------------------------------------------------------------ init (Alg.2 lines 1-10)
-__global__ void k_seed_root(uint32_t* vd, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
+__global__ void k_seed_root(uint32_t* vis, uint32_t* vold, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
                             const uint32_t* fwd_own, uint64_t t0, uint64_t block, int i, uint32_t root, int j) {
   const uint64_t t = fwd_own[t0];  // relabeled offset of the root in its block
   const uint64_t row_local = (uint64_t)j * block + t, col_local = (uint64_t)i * block + t;
-  vd[2 * (row_local >> 5)] |= 1u << (row_local & 31);   // bmap[LOCAL_ROW(r)] <- 1
+  vis[row_local >> 5] |= 1u << (row_local & 31);   // bmap[LOCAL_ROW(r)] <- 1
+  vold[row_local >> 5] |= 1u << (row_local & 31);
   all_front[col_local >> 5] |= 1u << (col_local & 31);  // front[0] <- LOCAL_COL(r)
   level[t] = 0;                                          // level[LOCAL_ROW(r)] <- 0
   pred[row_local] = root;                                // pred[LOCAL_ROW(r)] <- r
@@ -111,13 +102,14 @@ __global__ void k_seed_root(uint32_t* vd, uint32_t* all_front, int32_t* level, u
 // reader masks with the visited bit (unreached -> -1).
 cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s) {
   const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
-  cudaError_t e = cudaMemsetAsync(rk.vd, 0, 2 * rw * 4, s);
+  cudaError_t e = cudaMemsetAsync(rk.vis, 0, rw * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(rk.vold, 0, rw * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(rk.all_front, 0, cw * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(&rk.info->disc_total, 0, sizeof(ull), s);
   if (e != cudaSuccess) return e;
   if (owner) {
     const uint64_t t = root - (uint64_t)rk.r * g.block;
-    k_seed_root<<<1, 1, 0, s>>>(rk.vd, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
+    k_seed_root<<<1, 1, 0, s>>>(rk.vis, rk.vold, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
                                 (uint32_t)root, rk.j);
   }
   return cudaGetLastError();
@@ -637,85 +629,92 @@ __device__ __forceinline__ uint32_t hot_word(const uint32_t* s_hot, uint32_t v, 
 // (32-bit shared address sa, SEG1 layout: hw words + sentinel), then, if the row is neither hot
 // and visited nor invalid (pos >= len), one 8-byte L2 load of its visited|discovered pair.
 // Outputs: need (0/1), the bit mask m, the pair x|y and the pair's address for the RED.
-#ifndef BFS200_PROBE_LD
-#define BFS200_PROBE_LD "ld.global.cg.v2.u32"
-#endif
+// `vis` holds the visited bits of the level start ORed with the rows discovered so far in this
+// level (the RED.ORs go into the same word), so one 4-byte load both tests "visited" and
+// de-duplicates the REDs; `vold` keeps the level-start bits (K4 / K2 take the discovered word as
+// vis & ~vold).  A 128-byte line covers 1024 rows: lanes probing nearby rows of one column share
+// L2 requests (the L2 tag rate bounds the peak level).
 struct Probe {
-  uint32_t x, y, need, m;
+  uint32_t x, need, m;
   uint32_t* a;
 };
 __device__ __forceinline__ void probe_seg1(Probe& p, uint32_t v, uint32_t pos, uint32_t len, uint32_t hw, uint32_t sa,
-                                           uint32_t* vd) {
+                                           uint32_t* vis) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv;\n"
-      " setp.lt.u32 pok, %6, %7;\n"
-      " shr.b32 wi, %5, 5;\n"
-      " min.u32 hi, wi, %8;\n"
+      " setp.lt.u32 pok, %5, %6;\n"
+      " shr.b32 wi, %4, 5;\n"
+      " min.u32 hi, wi, %7;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %9;\n"
+      " add.u32 hi, hi, %8;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 %3, 0, 1, %5;\n"
-      " and.b32 hv, hv, %3;\n"
+      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
+      " and.b32 hv, hv, %2;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 %4, wi, 8, %10;\n"
-      " @pn " BFS200_PROBE_LD " {%0, %1}, [%4];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
+      " mad.wide.u32 %3, wi, 4, %9;\n"
+      " @pn ld.global.cg.u32 %0, [%3];\n"
+      " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(p.x), "=r"(p.y), "=r"(p.need), "=r"(p.m), "=l"(p.a)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
+      : "=r"(p.x), "=r"(p.need), "=r"(p.m), "=l"(p.a)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis));
 }
 // general layout (C row segments of hw words + sentinel each)
 __device__ __forceinline__ void probe_segs(Probe& p, uint32_t v, uint32_t pos, uint32_t len, uint32_t hw, uint32_t sa,
-                                           uint32_t* vd, int bl, uint32_t bmask) {
+                                           uint32_t* vis, int bl, uint32_t bmask) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, sg, off;\n"
-      " setp.lt.u32 pok, %6, %7;\n"
-      " shr.b32 wi, %5, 5;\n"
-      " shr.b32 sg, %5, %11;\n"
-      " and.b32 off, %5, %12;\n"
+      " setp.lt.u32 pok, %5, %6;\n"
+      " shr.b32 wi, %4, 5;\n"
+      " shr.b32 sg, %4, %10;\n"
+      " and.b32 off, %4, %11;\n"
       " shr.b32 off, off, 5;\n"
-      " min.u32 off, off, %8;\n"
-      " add.u32 hv, %8, 1;\n"
+      " min.u32 off, off, %7;\n"
+      " add.u32 hv, %7, 1;\n"
       " mad.lo.u32 hi, sg, hv, off;\n"
-      " selp.u32 hi, hi, %8, pok;\n"
+      " selp.u32 hi, hi, %7, pok;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %9;\n"
+      " add.u32 hi, hi, %8;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 %3, 0, 1, %5;\n"
-      " and.b32 hv, hv, %3;\n"
+      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
+      " and.b32 hv, hv, %2;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 %4, wi, 8, %10;\n"
-      " @pn " BFS200_PROBE_LD " {%0, %1}, [%4];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
+      " mad.wide.u32 %3, wi, 4, %9;\n"
+      " @pn ld.global.cg.u32 %0, [%3];\n"
+      " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(p.x), "=r"(p.y), "=r"(p.need), "=r"(p.m), "=l"(p.a)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+      : "=r"(p.x), "=r"(p.need), "=r"(p.m), "=l"(p.a)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
 }
-// RED.OR of the discovered bit if the probe was needed and neither bit is set (Alg.3 line 7)
+// RED.OR of the row's bit if the probe was needed and found it neither visited nor discovered
+// (Alg.3 line 7)
 __device__ __forceinline__ void probe_red(const Probe& p) {
   asm volatile("{\n"
                " .reg .pred pn, pr;\n"
                " .reg .b32 t;\n"
-               " setp.ne.b32 pn, %3, 0;\n"
-               " lop3.b32 t, %0, %1, %2, 0xa8;\n"
+               " setp.ne.b32 pn, %2, 0;\n"
+               " and.b32 t, %0, %1;\n"
                " setp.eq.and.b32 pr, t, 0, pn;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [%4+4], %2;\n"
-               "}" ::"r"(p.x), "r"(p.y), "r"(p.m), "r"(p.need), "l"(p.a));
+               " @pr red.relaxed.gpu.global.or.b32 [%3], %1;\n"
+               "}" ::"r"(p.x), "r"(p.m), "r"(p.need), "l"(p.a));
 }
 
-// One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows
-// against the shared-memory copy, the others with one 8-byte load of the visited|discovered
-// pair), then the discovered bit by RED.OR and, in P1 levels, the parent claim.
+// One warp tile's edges after their row ids v[] are loaded: the visited test (hot rows against
+// the shared-memory copy, the others with one 4-byte load), then the RED.OR of the row's bit and,
+// in P1 levels, the parent claim.  P1 levels test the LEVEL-START bits (vold): every frontier
+// neighbour of a row not visited before the level must claim it (the minimum decides), even when
+// another edge discovered the row earlier in this level; their RED.ORs into vis are then not
+// de-duplicated (P1 levels are the sparse ones).  P2 levels test vis (visited or discovered).
 // claim3 (P1 levels with a dense claim, mode 3): the claim alone, atomicMin of pmin; rows of the
-// hot prefix need no probe (their visited bit is exact in shared memory) and no discovered bit
-// is set here -- k_parent derives the discovered words from pmin.
+// hot prefix need no probe (their visited bit is exact in shared memory) and no bit is set here
+// -- k_parent derives the discovered words from pmin.
 template <int WV, bool P1, bool SEG1>
-__device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vd,
-                                             uint32_t* pmin, const uint32_t* s_hot, uint32_t bmask, int bl,
-                                             uint32_t hw, bool claim3 = false, bool blind3 = false) {
-  uint32_t wx[WV], wy[WV];
+__device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint32_t (&ug)[WV], uint32_t* vis,
+                                             const uint32_t* vold, uint32_t* pmin, const uint32_t* s_hot,
+                                             uint32_t bmask, int bl, uint32_t hw, bool claim3 = false,
+                                             bool blind3 = false) {
+  uint32_t wx[WV];
   bool need[WV], probe[WV];
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
@@ -729,14 +728,14 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
       // claim3: hot rows are decided already; blind3: the other rows claim without a probe
       probe[q] = need[q] && !(claim3 && (blind3 || off < hw * 32u));
     }
-    ld_cg_u2_p(probe[q], vd + 2 * (v[q] >> 5), wx[q], wy[q]);
+    ld_cg_u32_p(probe[q], (P1 ? vold : vis) + (v[q] >> 5), wx[q]);
   }
 #pragma unroll
   for (int q = 0; q < WV; ++q) {
     const uint32_t m = 1u << (v[q] & 31);
     const bool cand = need[q] && !(probe[q] && (wx[q] & m));  // not visited (Alg.3 lines 5-6)
     if (P1 && cand) atomicMin(pmin + v[q], ug[q]);  // parent claim: minimum original id (R1)
-    if (!claim3) red_or_if(cand && !(wy[q] & m), vd + 2 * (v[q] >> 5) + 1, m);  // Alg.3 line 7
+    if (!claim3) red_or_if(cand, vis + (v[q] >> 5), m);  // Alg.3 line 7
   }
 }
 
@@ -761,75 +760,74 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 // Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
 // keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
 // word address from v (two instructions instead of three live registers per row).
-__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
-                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd) {
+__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& need, uint32_t v, uint32_t pos, uint32_t len,
+                                            uint32_t hw, uint32_t sa, const uint32_t* vis) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, m;\n"
       " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %4, %5;\n"
-      " shr.b32 wi, %3, 5;\n"
-      " min.u32 hi, wi, %6;\n"
+      " setp.lt.u32 pok, %3, %4;\n"
+      " shr.b32 wi, %2, 5;\n"
+      " min.u32 hi, wi, %5;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %7;\n"
+      " add.u32 hi, hi, %6;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " shf.l.wrap.b32 m, 0, 1, %2;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %8;\n"
-      " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
+      " mad.wide.u32 a, wi, 4, %7;\n"
+      " @pn ld.global.cg.u32 %0, [a];\n"
+      " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd));
+      : "=r"(x), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis));
 }
-__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& y, uint32_t& need, uint32_t v, uint32_t pos,
-                                            uint32_t len, uint32_t hw, uint32_t sa, const uint32_t* vd, int bl,
-                                            uint32_t bmask) {
+__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& need, uint32_t v, uint32_t pos, uint32_t len,
+                                            uint32_t hw, uint32_t sa, const uint32_t* vis, int bl, uint32_t bmask) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
       " .reg .b32 wi, hi, hv, sg, off, m;\n"
       " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %4, %5;\n"
-      " shr.b32 wi, %3, 5;\n"
-      " shr.b32 sg, %3, %9;\n"
-      " and.b32 off, %3, %10;\n"
+      " setp.lt.u32 pok, %3, %4;\n"
+      " shr.b32 wi, %2, 5;\n"
+      " shr.b32 sg, %2, %8;\n"
+      " and.b32 off, %2, %9;\n"
       " shr.b32 off, off, 5;\n"
-      " min.u32 off, off, %6;\n"
-      " add.u32 hv, %6, 1;\n"
+      " min.u32 off, off, %5;\n"
+      " add.u32 hv, %5, 1;\n"
       " mad.lo.u32 hi, sg, hv, off;\n"
-      " selp.u32 hi, hi, %6, pok;\n"
+      " selp.u32 hi, hi, %5, pok;\n"
       " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %7;\n"
+      " add.u32 hi, hi, %6;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %3;\n"
+      " shf.l.wrap.b32 m, 0, 1, %2;\n"
       " and.b32 hv, hv, m;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 8, %8;\n"
-      " @pn " BFS200_PROBE_LD " {%0, %1}, [a];\n"
-      " selp.u32 %2, 1, 0, pn;\n"
+      " mad.wide.u32 a, wi, 4, %7;\n"
+      " @pn ld.global.cg.u32 %0, [a];\n"
+      " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(y), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vd), "r"(bl), "r"(bmask));
+      : "=r"(x), "=r"(need)
+      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
 }
-__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t y, uint32_t need, uint32_t* vd) {
+__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t need, uint32_t* vis) {
   asm volatile("{\n"
                " .reg .pred pn, pr;\n"
                " .reg .b32 t, m, wi;\n"
                " .reg .b64 a;\n"
-               " setp.ne.b32 pn, %3, 0;\n"
+               " setp.ne.b32 pn, %2, 0;\n"
                " shf.l.wrap.b32 m, 0, 1, %0;\n"
-               " lop3.b32 t, %1, %2, m, 0xa8;\n"
+               " and.b32 t, %1, m;\n"
                " setp.eq.and.b32 pr, t, 0, pn;\n"
                " shr.b32 wi, %0, 5;\n"
-               " mad.wide.u32 a, wi, 8, %4;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [a+4], m;\n"
-               "}" ::"r"(v), "r"(x), "r"(y), "r"(need), "l"(vd));
+               " mad.wide.u32 a, wi, 4, %3;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [a], m;\n"
+               "}" ::"r"(v), "r"(x), "r"(need), "l"(vis));
 }
 
 template <int E, bool SEG1, bool POS32, int NS>
 __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
-                                           uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vd, uint32_t hw,
+                                           uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vis, uint32_t hw,
                                            uint32_t sa, int bl, uint32_t bmask, int lane, const LevelInfo* info) {
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
   uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
@@ -871,17 +869,17 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
       const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (its record is loaded)
       rows_issue(sn);
       rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
-      uint32_t x[E], y[E], need[E];
+      uint32_t x[E], need[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) BCHECK(v[p][e] == 0xFFFFFFFFu || v[p][e] < info->cap_nrows);
 #pragma unroll
       for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
         const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
-        if (SEG1) probe2_seg1(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd);
-        else probe2_segs(x[e], y[e], need[e], v[p][e], pos, 1u, hw, sa, vd, bl, bmask);
+        if (SEG1) probe2_seg1(x[e], need[e], v[p][e], pos, 1u, hw, sa, vis);
+        else probe2_segs(x[e], need[e], v[p][e], pos, 1u, hw, sa, vis, bl, bmask);
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], y[e], need[e], vd);  // Alg.3 line 7
+      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], need[e], vis);  // Alg.3 line 7
       t += stride;
     }
   }
@@ -892,7 +890,8 @@ template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
                                             const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
-                                            ull nA, ull n, ull total, ull all_edges, uint32_t* vd, uint32_t* pmin,
+                                            ull nA, ull n, ull total, ull all_edges, uint32_t* vis,
+                                            const uint32_t* __restrict__ vold, uint32_t* pmin,
                                             const uint32_t* __restrict__ inv_col, uint32_t hot_words, int C,
                                             uint64_t W, int blog, uint32_t region_words, bool claim3,
                                             bool blind3, const LevelInfo* info) {
@@ -924,7 +923,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     const uint32_t hs = hw + 1;
     for (uint32_t k = threadIdx.x; k < (uint32_t)C * hs; k += THREADS) {
       const uint32_t m = k / hs, w = k - m * hs;
-      s_region[k] = w < hw ? vd[2 * ((uint64_t)m * W + w)] : 0u;
+      s_region[k] = w < hw ? vold[(uint64_t)m * W + w] : 0u;  // level-start visited bits
     }
   }
   __syncthreads();
@@ -964,13 +963,13 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           uint32_t ug[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) ug[q] = ug0;
-          expand_edges<LWV, true, SEG1>(vw, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
+          expand_edges<LWV, true, SEG1>(vw, ug, vis, vold, pmin, s_hot, bmask, bl, hw, claim3, blind3);
         } else {
           Probe pr[LWV];
 #pragma unroll
           for (int q = 0; q < LWV; ++q) {  // Alg.3 lines 5-6
-            if (SEG1) probe_seg1(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vd);
-            else probe_segs(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vd, bl, bmask);
+            if (SEG1) probe_seg1(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vis);
+            else probe_segs(pr[q], vw[q], 32u * (LWV * wv + q) + lane, r.z, hw, sa, vis, bl, bmask);
           }
 #pragma unroll
           for (int q = 0; q < LWV; ++q) probe_red(pr[q]);
@@ -979,7 +978,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
     if constexpr (!P1 && BFS200_K1PIPE > 0 && E <= 8) {
-      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE>(row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vd, hw, sa,
+      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE>(row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vis, hw, sa,
                                                     bl, bmask, lane, info);
     } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
@@ -1087,8 +1086,8 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
         Probe pr[LWV];
 #pragma unroll
         for (int q = 0; q < LWV; ++q) {  // Alg.3 lines 5-6
-          if (SEG1) probe_seg1(pr[q], v[q], 0u, 1u, hw, sa, vd);
-          else probe_segs(pr[q], v[q], 0u, 1u, hw, sa, vd, bl, bmask);
+          if (SEG1) probe_seg1(pr[q], v[q], 0u, 1u, hw, sa, vis);
+          else probe_segs(pr[q], v[q], 0u, 1u, hw, sa, vis, bl, bmask);
         }
 #pragma unroll
         for (int q = 0; q < LWV; ++q) probe_red(pr[q]);
@@ -1108,7 +1107,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = u0;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
+        expand_edges<WV, P1, SEG1>(v, ug, vis, vold, pmin, s_hot, bmask, bl, hw, claim3, blind3);
       }
     } else {
       // lane-interleaved edges e = 32q + lane; lane state: the staged column idx holding its
@@ -1155,7 +1154,7 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
           ug[q] = P1 ? s_u[idx] : 0u;
         }
         if (wv == 0) prefetch_next();
-        expand_edges<WV, P1, SEG1>(v, ug, vd, pmin, s_hot, bmask, bl, hw, claim3, blind3);
+        expand_edges<WV, P1, SEG1>(v, ug, vis, vold, pmin, s_hot, bmask, bl, hw, claim3, blind3);
       }
     }
     if (!rnext) {
@@ -1176,19 +1175,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restric
                                                        const ull* __restrict__ cumul,
                                                        const uint32_t* __restrict__ tile_k,
                                                        const uint4* __restrict__ tileA,
-                                                       const LevelInfo* __restrict__ info, uint32_t* vd,
+                                                       const LevelInfo* __restrict__ info, uint32_t* vis,
+                                                       const uint32_t* __restrict__ vold,
                                                        uint32_t* pmin, const uint32_t* __restrict__ inv_col,
                                                        uint32_t hot_words, int C, uint64_t W, int blog,
                                                        uint32_t region_words) {
   const ull n = info->n, total = info->sedges, nA = info->nA, all_edges = info->edges;
   if (all_edges == 0) return;
   if (info->mode != 2)
-    expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vd,
-                                               pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3,
+    expand_body<E, THREADS, true, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges, vis,
+                                               vold, pmin, inv_col, hot_words, C, W, blog, region_words, info->mode == 3,
                                                info->blind != 0, info);
   else
     expand_body<E, THREADS, false, SEG1, POS32>(row, flist, rowoff, cumul, tile_k, tileA, nA, n, total, all_edges,
-                                                vd, pmin, inv_col, hot_words, C, W, blog, region_words, false, false, info);
+                                                vis, vold, pmin, inv_col, hot_words, C, W, blog, region_words, false, false,
+                                                info);
 }
 
 template <int E, int THREADS>
@@ -1219,7 +1220,7 @@ static cudaError_t launch_expand_t(const Geom& g, Rank& rk, uint64_t hot_h, bool
   const size_t smem = staging + region + 16;
   auto kern = g.C == 1 ? (pos32 ? k_expand<E, THREADS, true, true> : k_expand<E, THREADS, true, false>)
                        : (pos32 ? k_expand<E, THREADS, false, true> : k_expand<E, THREADS, false, false>);
-  kern<<<g.nsm, THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vd,
+  kern<<<g.nsm, THREADS, smem, s>>>(rk.row, rk.flist, rk.rowoff, rk.cumul, rk.tile_k, rk.tileA, rk.info, rk.vis, rk.vold,
                                         rk.pmin, rk.inv_col, (uint32_t)hw, g.C, g.words_block(), blog,
                                         (uint32_t)(region / 4));
   return cudaGetLastError();
@@ -1274,7 +1275,8 @@ constexpr int kLaneStep = BFS200_LANE_STEP;  // CSR entries per lane step (loads
 constexpr int kParRows = BFS200_PAR_ROWS;  // P2 rows scanned together per lane
 constexpr size_t kParentHotSmem = 64 * 1024;  // hot prefix of the frontier bitmap (P2 levels)
 
-__global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint64_t nwords,
+__global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, const uint32_t* __restrict__ vold,
+                                                               uint64_t nwords,
                                                                const ull* __restrict__ csr_ptr,
                                                                const uint32_t* __restrict__ csr_col,
                                                                const uint32_t* __restrict__ front, uint32_t* pred,
@@ -1314,7 +1316,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
       uint32_t myd = 0;
       const int nk = (int)min((uint64_t)32, nwords - ch * 32);
       // visited words of the chunk (blind claims may have reached visited rows: not discovered)
-      const uint32_t visw = (blind && w < nwords) ? vd[2 * w] : 0u;
+      const uint32_t visw = (blind && w < nwords) ? vold[w] : 0u;
       // 16 rows' pmin loads in flight per lane (a streaming pass: bytes in flight set its speed)
 #pragma unroll 1
       for (int k0 = 0; k0 < nk; k0 += 16) {
@@ -1336,7 +1338,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
         }
       }
       if (w < nwords) {
-        vd[2 * w + 1] = myd;
+        vis[w] = vold[w] | myd;  // mode 3 sets no bit in K1: the level's discoveries enter here
         if (sendbuf) sendbuf[w] = myd;
         if (fold_dst) {  // peer exchange: the fold message goes straight into the owner's recv
           const uint64_t c = w / Wc;
@@ -1346,7 +1348,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vd, uint
       ndisc += __popc(myd);
       continue;
     }
-    const uint32_t d = (w < nwords) ? vd[2 * w + 1] : 0u;
+    const uint32_t d = (w < nwords) ? (vis[w] & ~vold[w]) : 0u;  // rows discovered in this level
     if (sendbuf && w < nwords) sendbuf[w] = d;
     if (fold_dst && w < nwords) {  // peer exchange (NVLink stores): segment c -> recv of P_ic
       const uint64_t c = w / Wc;
@@ -1489,7 +1491,7 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   if (hw > g.words_block()) hw = g.words_block();
   if (blog < 0) hw = 0;
   const size_t smem = (size_t)(kParentThreads / 32) * 1024 * 4 + (size_t)(g.R * hw > 4 ? g.R * hw : 4) * 4;
-  k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vd, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
+  k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vis, rk.vold, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
                                                         rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
                                                         (uint32_t)hw, g.R, g.words_block(), blog,
                                                         g.C > 1 ? rk.fold_dst : nullptr);
@@ -1515,7 +1517,8 @@ cudaError_t kernels_init_device() {
 // rows received from any column (own discoveries included) that are not yet visited; the
 // lowest sending column is recorded as the parent's column (winner).  Other segments: mark the
 // rows this rank discovered as visited so they are sent at most once.
-__global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* recv, uint32_t* front_seg,
+__global__ void __launch_bounds__(256) k_update(uint32_t* vis, uint32_t* vold, const uint32_t* recv,
+                                                uint32_t* front_seg,
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
                                                 int j, const LevelCtrl* ctrl, uint32_t* const* __restrict__ exp_dst,
                                                 int R) {
@@ -1530,11 +1533,10 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
     uint32_t newbits = 0;
     uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
     if (m == j && w < W) {
-      const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
-      const uint32_t vis = p.x;
+      const uint32_t vo = vold[gid], own = vis[gid] & ~vo;  // level-start bits, own discoveries
       uint32_t claimed = 0;
       for (int c = 0; c < C; ++c) {
-        const uint32_t x = ((c == j) ? p.y : recv[(uint64_t)c * W + w]) & ~vis & ~claimed;
+        const uint32_t x = ((c == j) ? own : recv[(uint64_t)c * W + w]) & ~vo & ~claimed;
         if (c < 8) wbits[c] = x;
         if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
           uint32_t b = x;
@@ -1546,15 +1548,15 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vd, const uint32_t* re
         }
         claimed |= x;
       }
-      newbits = claimed;
-      if (newbits | p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(vis | newbits, 0u);
+      newbits = claimed;  // includes own (own discoveries were not visited at the level start)
+      if (newbits) vis[gid] = vold[gid] = vo | newbits;
       front_seg[w] = newbits;
       if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
         for (int i2 = 0; i2 < R; ++i2)
           if (exp_dst[i2]) exp_dst[i2][w] = newbits;
-    } else if (w < W) {
-      const uint2 p = *reinterpret_cast<const uint2*>(vd + 2 * gid);
-      if (p.y) *reinterpret_cast<uint2*>(vd + 2 * gid) = make_uint2(p.x | p.y, 0u);
+    } else if (w < W) {  // rows of other owners discovered here stay visited on this rank
+      const uint32_t vn = vis[gid];
+      if (vn != vold[gid]) vold[gid] = vn;
     }
     // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing vertex
     // 32k + l of word k (coalesced stores instead of per-bit scattered ones)
@@ -1594,7 +1596,7 @@ cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaSt
   const uint64_t cap = (uint64_t)g.nsm * 8 / (uint64_t)g.C;
   if (g.R > 1 && rk.exp_dst && gx > cap) gx = cap ? cap : 1;
   const dim3 grid((unsigned)gx, (unsigned)g.C);
-  k_update<<<grid, 256, 0, s>>>(rk.vd, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
+  k_update<<<grid, 256, 0, s>>>(rk.vis, rk.vold, rk.recv, rk.all_front + (uint64_t)rk.i * W, rk.level,
                                 g.C > 1 ? rk.winner : nullptr, rk.info, W, g.C, rk.j, ctrl,
                                 g.R > 1 ? rk.exp_dst : nullptr, g.R);
   return cudaGetLastError();
@@ -1660,7 +1662,7 @@ cudaError_t launch_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal
 // whose winner column c differs from j takes its parent from the answers of P_ic: position =
 // rank of its bit among the requests sent to c (exclusive popcount scan off_req + in-word popc).
 struct FinalizeArgs {
-  const uint32_t* vd_own;
+  const uint32_t* vis_own;
   const int32_t* level;
   const uint32_t* pred_own;
   const uint8_t* winner;  // null when C == 1
@@ -1683,7 +1685,7 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
   for (int k = 0; k < 4; ++k) {
     const uint32_t p = pp[k];
     BCHECK(p < a.block);
-    const bool reached = (a.vd_own[2 * (p >> 5)] >> (p & 31)) & 1u;
+    const bool reached = (a.vis_own[p >> 5] >> (p & 31)) & 1u;
     int64_t v = -1;
     if (reached && parent_out) {  // without a parent output the resolution did not run
       const int c = a.winner ? (int)a.winner[p] : a.j;
@@ -1709,7 +1711,7 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
 
 cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
   FinalizeArgs a;
-  a.vd_own = rk.vd + 2 * (uint64_t)rk.j * g.words_block();
+  a.vis_own = rk.vis + (uint64_t)rk.j * g.words_block();
   a.level = rk.level;
   a.pred_own = rk.pred + (uint64_t)rk.j * g.block;
   a.winner = (g.C > 1 && parent_out) ? rk.winner : nullptr;  // parents of other columns need resolution
@@ -1727,10 +1729,10 @@ cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_
 
 // ------------------------------------------------------------------ parent resolution (C > 1)
 // request bitmaps: req[c] has bit t for owned reached t whose winner column is c != j
-__global__ void k_req_build(const uint32_t* vd_own, const uint8_t* winner, uint32_t* req, uint64_t W, int C, int j) {
+__global__ void k_req_build(const uint32_t* vis_own, const uint8_t* winner, uint32_t* req, uint64_t W, int C, int j) {
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= W) return;
-  uint32_t b = vd_own[2 * w];  // visited word
+  uint32_t b = vis_own[w];  // visited word
   while (b) {
     const int bit = __ffs(b) - 1;
     b &= b - 1;
@@ -1742,7 +1744,7 @@ __global__ void k_req_build(const uint32_t* vd_own, const uint8_t* winner, uint3
 cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t W = g.words_block();
   cudaMemsetAsync(rk.req, 0, W * g.C * 4, s);
-  k_req_build<<<(unsigned)((W + 255) / 256), 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * W, rk.winner, rk.req, W,
+  k_req_build<<<(unsigned)((W + 255) / 256), 256, 0, s>>>(rk.vis + (uint64_t)rk.j * W, rk.winner, rk.req, W,
                                                            g.C, rk.j);
   return cudaGetLastError();
 }
@@ -1836,19 +1838,19 @@ cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ m_comp, degree
-__global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vd_own, const uint32_t* tdeg, const uint32_t* fwd_own,
+__global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vis_own, const uint32_t* tdeg, const uint32_t* fwd_own,
                                                uint64_t block, ull* out) {
   typedef cub::BlockReduce<ull, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   ull acc = 0;
   for (uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x; t < block; t += (uint64_t)gridDim.x * 256)
-    if ((vd_own[2 * (fwd_own[t] >> 5)] >> (fwd_own[t] & 31)) & 1u) acc += tdeg[t];
+    if ((vis_own[fwd_own[t] >> 5] >> (fwd_own[t] & 31)) & 1u) acc += tdeg[t];
   ull tot = BR(tmp).Sum(acc);
   if (threadIdx.x == 0 && tot) atomicAdd(out, tot);
 }
 
 cudaError_t launch_mcomp(const Geom& g, Rank& rk, ull* out, cudaStream_t s) {
-  k_mcomp<<<g.nsm * 4, 256, 0, s>>>(rk.vd + 2 * (uint64_t)rk.j * g.words_block(), rk.tdeg, rk.fwd_own, g.block,
+  k_mcomp<<<g.nsm * 4, 256, 0, s>>>(rk.vis + (uint64_t)rk.j * g.words_block(), rk.tdeg, rk.fwd_own, g.block,
                                          out);
   return cudaGetLastError();
 }
