@@ -760,38 +760,39 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 // Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
 // keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
 // word address from v (two instructions instead of three live registers per row).
-__device__ __forceinline__ void probe2_seg1(uint32_t& x, uint32_t& need, uint32_t v, uint32_t pos, uint32_t len,
-                                            uint32_t hw, uint32_t sa, const uint32_t* vis) {
+// Probe and RED of one row of a long tile (the hot loop of the peak level): the probe returns the
+// loaded visited word, the need flag, the row's bit mask and its word address, and the RED reuses
+// them; the lane's validity is the row sentinel (0xFFFFFFFF past a tile's end).
+__device__ __forceinline__ void probe4_seg1(uint32_t& x, uint32_t& need, uint32_t& m, uint32_t*& a, uint32_t v,
+                                            uint32_t hw, uint32_t sa, uint32_t* vis) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
-      " .reg .b32 wi, hi, hv, m;\n"
-      " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %3, %4;\n"
-      " shr.b32 wi, %2, 5;\n"
+      " .reg .b32 wi, hi, hv;\n"
+      " setp.ne.u32 pok, %4, 0xFFFFFFFF;\n"
+      " shr.b32 wi, %4, 5;\n"
       " min.u32 hi, wi, %5;\n"
       " shl.b32 hi, hi, 2;\n"
       " add.u32 hi, hi, %6;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %2;\n"
-      " and.b32 hv, hv, m;\n"
+      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
+      " and.b32 hv, hv, %2;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 4, %7;\n"
-      " @pn ld.global.cg.u32 %0, [a];\n"
+      " mad.wide.u32 %3, wi, 4, %7;\n"
+      " @pn ld.global.cg.u32 %0, [%3];\n"
       " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis));
+      : "=r"(x), "=r"(need), "=r"(m), "=l"(a)
+      : "r"(v), "r"(hw), "r"(sa), "l"(vis));
 }
-__device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& need, uint32_t v, uint32_t pos, uint32_t len,
-                                            uint32_t hw, uint32_t sa, const uint32_t* vis, int bl, uint32_t bmask) {
+__device__ __forceinline__ void probe4_segs(uint32_t& x, uint32_t& need, uint32_t& m, uint32_t*& a, uint32_t v,
+                                            uint32_t hw, uint32_t sa, uint32_t* vis, int bl, uint32_t bmask) {
   asm("{\n"
       " .reg .pred pok, pn;\n"
-      " .reg .b32 wi, hi, hv, sg, off, m;\n"
-      " .reg .b64 a;\n"
-      " setp.lt.u32 pok, %3, %4;\n"
-      " shr.b32 wi, %2, 5;\n"
-      " shr.b32 sg, %2, %8;\n"
-      " and.b32 off, %2, %9;\n"
+      " .reg .b32 wi, hi, hv, sg, off;\n"
+      " setp.ne.u32 pok, %4, 0xFFFFFFFF;\n"
+      " shr.b32 wi, %4, 5;\n"
+      " shr.b32 sg, %4, %8;\n"
+      " and.b32 off, %4, %9;\n"
       " shr.b32 off, off, 5;\n"
       " min.u32 off, off, %5;\n"
       " add.u32 hv, %5, 1;\n"
@@ -800,29 +801,25 @@ __device__ __forceinline__ void probe2_segs(uint32_t& x, uint32_t& need, uint32_
       " shl.b32 hi, hi, 2;\n"
       " add.u32 hi, hi, %6;\n"
       " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 m, 0, 1, %2;\n"
-      " and.b32 hv, hv, m;\n"
+      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
+      " and.b32 hv, hv, %2;\n"
       " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 a, wi, 4, %7;\n"
-      " @pn ld.global.cg.u32 %0, [a];\n"
+      " mad.wide.u32 %3, wi, 4, %7;\n"
+      " @pn ld.global.cg.u32 %0, [%3];\n"
       " selp.u32 %1, 1, 0, pn;\n"
       "}"
-      : "=r"(x), "=r"(need)
-      : "r"(v), "r"(pos), "r"(len), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
+      : "=r"(x), "=r"(need), "=r"(m), "=l"(a)
+      : "r"(v), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
 }
-__device__ __forceinline__ void red2(uint32_t v, uint32_t x, uint32_t need, uint32_t* vis) {
+__device__ __forceinline__ void red4(uint32_t x, uint32_t need, uint32_t m, uint32_t* a) {
   asm volatile("{\n"
                " .reg .pred pn, pr;\n"
-               " .reg .b32 t, m, wi;\n"
-               " .reg .b64 a;\n"
-               " setp.ne.b32 pn, %2, 0;\n"
-               " shf.l.wrap.b32 m, 0, 1, %0;\n"
-               " and.b32 t, %1, m;\n"
+               " .reg .b32 t;\n"
+               " setp.ne.b32 pn, %1, 0;\n"
+               " and.b32 t, %0, %2;\n"
                " setp.eq.and.b32 pr, t, 0, pn;\n"
-               " shr.b32 wi, %0, 5;\n"
-               " mad.wide.u32 a, wi, 4, %3;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [a], m;\n"
-               "}" ::"r"(v), "r"(x), "r"(need), "l"(vis));
+               " @pr red.relaxed.gpu.global.or.b32 [%3], %2;\n"
+               "}" ::"r"(x), "r"(need), "r"(m), "l"(a));
 }
 
 template <int E, bool SEG1, bool POS32, int NS>
@@ -872,14 +869,15 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
       uint32_t x[E], need[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) BCHECK(v[p][e] == 0xFFFFFFFFu || v[p][e] < info->cap_nrows);
+      uint32_t mk[E];
+      uint32_t* ad[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6 (a row of 0xFFFFFFFF is past the tile: pos 1 >= len 1)
-        const uint32_t pos = v[p][e] == 0xFFFFFFFFu ? 1u : 0u;
-        if (SEG1) probe2_seg1(x[e], need[e], v[p][e], pos, 1u, hw, sa, vis);
-        else probe2_segs(x[e], need[e], v[p][e], pos, 1u, hw, sa, vis, bl, bmask);
+      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
+        if (SEG1) probe4_seg1(x[e], need[e], mk[e], ad[e], v[p][e], hw, sa, vis);
+        else probe4_segs(x[e], need[e], mk[e], ad[e], v[p][e], hw, sa, vis, bl, bmask);
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) red2(v[p][e], x[e], need[e], vis);  // Alg.3 line 7
+      for (int e = 0; e < E; ++e) red4(x[e], need[e], mk[e], ad[e]);  // Alg.3 line 7
       t += stride;
     }
   }
