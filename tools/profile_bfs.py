@@ -40,5 +40,5 @@ for r in roots:
     for i, x in enumerate(recs):
         print(f"  L{i}: frontier {x.frontier:>10} edges {x.edges:>12} scan {x.scan:7.3f} expand {x.expand:7.3f} "
               f"parent {x.parent:6.3f} update {x.update:6.3f} ms  -> "
-              f"{((4*x.edges+20*x.frontier)/1e9)/(max(x.expand,1e-6)*1e-3):8.1f} GB/s")
+              f"{((4*x.edges+40*x.frontier)/1e9)/(max(x.expand,1e-6)*1e-3):8.1f} GB/s (4E+40F over K1)")
 g.close()
