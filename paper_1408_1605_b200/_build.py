@@ -94,12 +94,13 @@ def build_bfs(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_variant(name: str, defines, force: bool = False) -> str:
-    """An experiment build of the same library with extra -D flags (A/B runs through BFS200_LIB);
+def build_variant(name: str, defines, force: bool = False, csrc: str = CSRC, include: str = INCLUDE) -> str:
+    """An experiment build of the library with extra -D flags, or of another source tree (e.g. a
+    git revision exported by tools/build_rev.py), for A/B runs through BFS200_LIB;
     build/variants/lib<name>.so.  Never loaded unless BFS200_LIB points at it."""
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
-                  glob.glob(os.path.join(INCLUDE, "*.h")))
+    srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
+    hdrs = sorted(glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh")) +
+                  glob.glob(os.path.join(include, "*.h")))
     vdir = os.path.join(BUILD_DIR, "variants", name)
     out = os.path.join(BUILD_DIR, "variants", f"lib{name}.so")
     if not force and not _stale(out, srcs + hdrs):
@@ -111,7 +112,7 @@ def build_variant(name: str, defines, force: bool = False) -> str:
     for s in srcs:
         o = os.path.join(vdir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        jobs.append(([nvcc(), *ARCH, *NVCC_FLAGS, *dflags, "-I", INCLUDE, "-I", inc, "-c", s, "-o", o], o + ".log"))
+        jobs.append(([nvcc(), *ARCH, *NVCC_FLAGS, *dflags, "-I", include, "-I", inc, "-c", s, "-o", o], o + ".log"))
     with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
         list(ex.map(lambda a: _run(*a), jobs))
     _run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}",

@@ -768,6 +768,12 @@ static int resolve_parents(Graph& G) {
 // expand exchange, K3 scan, K1 expansion, K4 parent claim, fold exchange, K2 update,
 // termination all-reduce and the device-side level bookkeeping.  use_cond: the call is being
 // captured into the body of the CUDA-graph WHILE node (no phase events then).
+// 32-bit K3/K1 offsets when every CSC position of the rank fits (the same test as K1's POS32
+// variant; the test-only BFS_DEBUG_POS64 flag forces the 64-bit path in both)
+static bool narrow_of(const Graph& G, const Rank& rk) {
+  return rk.nnz < (1ull << 32) && !(G.opts.debug_flags & BFS_DEBUG_POS64);
+}
+
 static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const Geom& g = G.g;
   cudaStream_t s = G.stream;
@@ -781,7 +787,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
     Rank& rk = G.ranks[0];
     if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
     if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
-    CKR(launch_scan(g, rk, tile_edges, s));
+    CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), s));
     if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
     CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
     if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
@@ -802,7 +808,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const bool xl = G.opts.exchange != BFS_XCHG_BITMAP;  // never inside a graph capture
   if ((rc = xl ? expand_exchange_x(G) : expand_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, s));
+  for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), s));
   if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
   if (ev && (rc = ev_rec(G, nlev, 3))) return rc;

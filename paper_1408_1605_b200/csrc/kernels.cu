@@ -284,7 +284,8 @@ __device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t
 }
 
 __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
-                                                               SegTot* seg_off, LevelInfo* info, ull* cumul, ull nnz,
+                                                               SegTot* seg_off, LevelInfo* info, void* cumul, int narrow,
+                                                               ull nnz,
                                                                ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
   __shared__ SegAcc s_warp[kSegScanThreads / 32];
   __shared__ SegAcc s_carry;
@@ -348,19 +349,26 @@ __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __re
   info->blind = (info->mode == 3 && kBlind3 && seen * 16ull <= nz_rows) ? 1ull : 0ull;
   info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
   info->nlongcols = 0;
-  cumul[c.cs] = c.ss;
+  if (narrow) static_cast<uint32_t*>(cumul)[c.cs] = (uint32_t)c.ss;
+  else static_cast<ull*>(cumul)[c.cs] = c.ss;
 }
 
 // Emit pass: same word ownership.  Sparse chunks (< 96 set bits in 32 words): each lane totals
 // its word, one warp exclusive scan per chunk gives the lane its list / edge / long-tile / hub
 // positions, then the lane writes its columns in ascending order.  Dense chunks: word by word,
 // lane b handles bit b (coalesced col reads and list writes), col loads of 4 words in flight.
+// NARROW (every CSC position < 2^32): the row offsets and the scan are stored as 32-bit values
+// (12 B per short column instead of 20, written here and read by K1).
+template <bool NARROW>
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                              uint64_t nseg, const ull* __restrict__ col,
                                                              const SegTot* seg_tot, const SegTot* cta_off,
-                                                             uint32_t* flist, ull* rowoff,
-                                                             ull* cumul, uint32_t* tile_k, uint4* tileA,
+                                                             uint32_t* flist, void* rowoff_v, void* cumul_v,
+                                                             uint32_t* tile_k, uint4* tileA,
                                                              int tile_shift, uint4* longlist, LevelInfo* info) {
+  typedef typename std::conditional<NARROW, uint32_t, ull>::type Off;
+  Off* rowoff = static_cast<Off*>(rowoff_v);
+  Off* cumul = static_cast<Off*>(cumul_v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
   if (seg >= nseg) return;
@@ -451,8 +459,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
             const ull eb = e + inc - ds;
             BCHECK(pos < info->cap_ncols && u < info->cap_ncols && c0 + ds <= info->cap_nnz);
             flist[pos] = (uint32_t)u;
-            rowoff[pos] = c0;
-            cumul[pos] = eb;
+            rowoff[pos] = (Off)c0;
+            cumul[pos] = (Off)eb;
             for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) {
               BCHECK(t < info->cap_nnz / 32 + 2);
               tile_k[t] = (uint32_t)pos;
@@ -530,8 +538,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
       } else if (d) {
         BCHECK(kk < info->cap_ncols && u < info->cap_ncols && c0 + d <= info->cap_nnz);
         flist[kk] = (uint32_t)u;
-        rowoff[kk] = c0;
-        cumul[kk] = ee;
+        rowoff[kk] = (Off)c0;
+        cumul[kk] = (Off)ee;
         for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) {
           BCHECK(t < info->cap_nnz / 32 + 2);
           tile_k[t] = (uint32_t)kk;
@@ -568,7 +576,7 @@ __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4*
   }
 }
 
-cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s) {
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, cudaStream_t s) {
   const uint64_t nwords = g.ncols() / 32;
   const uint64_t nseg = (nwords + kScanSegWords - 1) / kScanSegWords;
   const unsigned grid = (unsigned)((nseg + kScanThreads / 32 - 1) / (kScanThreads / 32));
@@ -578,10 +586,11 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream
   SegTot* co = ct + grid;
   k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts);
   // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
-  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
+  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
                                           kM3Factor, (ull)g.nrows());
-  k_scan_emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff,
-                                            rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
+  auto emit = narrow ? k_scan_emit<true> : k_scan_emit<false>;
+  emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff, rk.cumul,
+                                     rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
   return cudaGetLastError();
 }
@@ -886,7 +895,7 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
 
 template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
-                                            const ull* __restrict__ rowoff, const ull* __restrict__ cumul,
+                                            const void* __restrict__ rowoff_v, const void* __restrict__ cumul_v,
                                             const uint32_t* __restrict__ tile_k, const uint4* __restrict__ tileA,
                                             ull nA, ull n, ull total, ull all_edges, uint32_t* vis,
                                             const uint32_t* __restrict__ vold, uint32_t* pmin,
@@ -903,6 +912,9 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   // staged row positions: 32-bit when every CSC position fits (nnz < 2^32; modular arithmetic
   // below stays exact), which leaves more of the SM's unified L1/shared memory to L1
   typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  // K3's row offsets and degree scan are 32-bit in the same case (k_scan_emit<NARROW>)
+  const Pos* __restrict__ rowoff = static_cast<const Pos*>(rowoff_v);
+  const Pos* __restrict__ cumul = static_cast<const Pos*>(cumul_v);
   unsigned char* wchunk = smem + (size_t)wid * expand_warp_bytes<E>(POS32);
   Pos* s_off = reinterpret_cast<Pos*>(wchunk);
   uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_off + SLOT);
@@ -1169,8 +1181,8 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
 template <int E, int THREADS, bool SEG1, bool POS32>
 __global__ void __launch_bounds__(THREADS, 1) k_expand(const uint32_t* __restrict__ row,
                                                        const uint32_t* __restrict__ flist,
-                                                       const ull* __restrict__ rowoff,
-                                                       const ull* __restrict__ cumul,
+                                                       const void* __restrict__ rowoff,
+                                                       const void* __restrict__ cumul,
                                                        const uint32_t* __restrict__ tile_k,
                                                        const uint4* __restrict__ tileA,
                                                        const LevelInfo* __restrict__ info, uint32_t* vis,
@@ -1288,6 +1300,10 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool p1 = info->mode == 1, m3 = info->mode == 3, blind = m3 && info->blind;
+  // parent candidate of local row r.  (Measured: the owned rows' candidates interleaved with
+  // their levels, so k_finalize gathers one 8-byte record per vertex: finalize -0.03 ms but the
+  // stride-2 writes of K4 and K2 +0.1 ms per BFS at s26 -- partial sectors; not kept.)
+  auto put_pred = [&](uint64_t r, uint32_t val) { pred[r] = val; };
   unsigned ndisc = 0;
   // P2: frontier bits of the hot (relabeled, highest-degree) column prefix of each of the R
   // column segments, so most frontier tests of the CSR scans stay in shared memory
@@ -1330,7 +1346,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
           const bool c = pm[q] != 0xFFFFFFFFu;
           const bool f = c && !((vk >> lane) & 1u);
           const unsigned dd = __ballot_sync(0xFFFFFFFFu, f);
-          if (f) pred[r] = pm[q];
+          if (f) put_pred(r, pm[q]);
           if (c) pmin[r] = 0xFFFFFFFFu;
           if (lane == k) myd = dd;
         }
@@ -1360,7 +1376,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
         const int bit = __ffs(b) - 1;
         b &= b - 1;
         const uint64_t r = w * 32 + bit;
-        pred[r] = pmin[r];
+        put_pred(r, pmin[r]);
         pmin[r] = 0xFFFFFFFFu;
       }
       continue;
@@ -1430,7 +1446,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
         if (r[i] == 0xFFFFFFFFu) continue;
         BCHECK(r[i] < nwords * 32 && (best[i] == 0xFFFFFFFFu || best[i] < info->cap_ncols));
         if (best[i] != 0xFFFFFFFFu) {
-          pred[r[i]] = pv[i];
+          put_pred(r[i], pv[i]);
         } else {  // defer to the whole warp; slot lane+32*nlong <= q0+32i was already read
           queue[wid][lane + 32 * nlong] = r[i];
           ++nlong;
@@ -1460,7 +1476,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
           }
         }
         BCHECK(best < info->cap_ncols);  // a discovered row has a frontier neighbour in its CSR row
-        if (lane == 0) pred[r] = inv_col[best];
+        if (lane == 0) put_pred(r, inv_col[best]);
       }
     }
     __syncwarp();

@@ -12,7 +12,9 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
 
 // K3: frontier bitmap (ncols bits) -> ascending list of columns with degree > 0, their row
 // offsets and the exclusive scan of their degrees.
-cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, cudaStream_t s);
+// narrow: every CSC position of the rank fits in 32 bits and K1 runs its POS32 variant (the row
+// offsets and the degree scan are then written as 32-bit values)
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, cudaStream_t s);
 
 // K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
 cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, bool force_pos64,
