@@ -75,6 +75,7 @@ struct Rank {
   uint64_t nnz = 0;   // CSC entries
   uint64_t nz_rows = 0;  // local rows with at least one entry (for the parent-mode heuristic)
   unsigned long long* col = nullptr;  // [ncols+1] column offsets (u64: nnz can exceed 2^32)
+  uint32_t* col32 = nullptr;          // [ncols+1] the same as u32 when nnz < 2^32 (read by K3)
   uint32_t* row = nullptr;    // [nnz] local row ids, ascending within each column
   // CSR view of the same local matrix (row -> ascending local columns) for the parent pass;
   // with R = C = 1 the matrix is symmetric and these alias col/row.

@@ -129,6 +129,11 @@ __global__ void k_perm_from_sorted(const uint32_t* sorted, uint64_t n, uint32_t*
   }
 }
 
+__global__ void k_narrow(const ull* in, uint64_t n, uint32_t* out) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    out[t] = (uint32_t)in[t];
+}
+
 // ---- CSC / CSR assembly
 // row[t] = the key's relabeled local row
 __global__ void k_keys_to_rows(const ull* keys, uint64_t n, int rbits, uint32_t* row) {
@@ -254,6 +259,12 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   const uint64_t nc = g.ncols() + 1;
   k_offsets<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(keys, rk.nnz, rbits, g.ncols(), rk.col);
   CKR(cudaGetLastError());
+  if (rk.nnz < (1ull << 32)) {  // 32-bit copy for the unpack / degree scan (K3 reads half the bytes)
+    rc = G_alloc(G, (void**)&rk.col32, nc * sizeof(uint32_t));
+    if (rc) return rc;
+    k_narrow<<<1024, 256, 0, s>>>(rk.col, nc, rk.col32);
+    CKR(cudaGetLastError());
+  }
   CKR(cudaStreamSynchronize(s));
   // CSR of the same local matrix for the parent pass (rows scanned in ascending ORIGINAL
   // column order; the CSC lists rows in relabeled order, so even a 1x1 grid needs its own copy)

@@ -137,8 +137,9 @@ struct SegTot {
 static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
 // Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
 // chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
+template <typename Col>
 __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uint64_t nwords, uint64_t seg,
-                                            const ull* __restrict__ col, int tile_shift) {
+                                            const Col* __restrict__ col, int tile_shift) {
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
@@ -189,7 +190,7 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
         for (int b = 0; b < 2; ++b) {
           const unsigned idx = g + 32 * b + lane;
           const uint64_t u = wb * 32 + (idx < nbits ? s_list[idx] : 0u);
-          dd[b] = idx < nbits ? __ldg(col + u + 1) - __ldg(col + u) : 0ull;
+          dd[b] = idx < nbits ? (ull)(__ldg(col + u + 1) - __ldg(col + u)) : 0ull;
         }
         add_col(dd[0]);
         add_col(dd[1]);
@@ -204,7 +205,7 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
         const int b = x ? __ffs(x) - 1 : -1;
         x &= x ? x - 1 : 0u;
         const uint64_t u = w * 32 + (b < 0 ? 0 : b);
-        dd[q] = b < 0 ? 0ull : __ldg(col + u + 1) - __ldg(col + u);
+        dd[q] = b < 0 ? 0ull : (ull)(__ldg(col + u + 1) - __ldg(col + u));
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) add_col(dd[q]);
@@ -224,8 +225,9 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
 // Per-segment totals (seg_tot[seg]) and per-CTA totals of the kScanThreads/32 segments of a CTA
 // (cta_tot[b]): the single-CTA scan (k_seg_scan) then only scans the few CTA totals, and the
 // emit pass adds the in-CTA prefix itself.
+template <typename Col>
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
-                                                              uint64_t nseg, const ull* __restrict__ col,
+                                                              uint64_t nseg, const Col* __restrict__ col,
                                                               SegTot* seg_tot, SegTot* cta_tot, int tile_shift) {
   __shared__ SegTot s_t[kScanThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -361,7 +363,9 @@ __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __re
 // (12 B per short column instead of 20, written here and read by K1).
 template <bool NARROW>
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ bm, uint64_t nwords,
-                                                             uint64_t nseg, const ull* __restrict__ col,
+                                                             uint64_t nseg,
+                                                             const typename std::conditional<NARROW, uint32_t, ull>::type*
+                                                                 __restrict__ col,
                                                              const SegTot* seg_tot, const SegTot* cta_off,
                                                              uint32_t* flist, void* rowoff_v, void* cumul_v,
                                                              uint32_t* tile_k, uint4* tileA,
@@ -431,8 +435,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
           const unsigned idx = g + 32 * b + lane;
           const bool valid = idx < nbits;
           ub[b] = wb * 32 + (valid ? s_list[idx] : 0u);
-          c0b[b] = valid ? __ldg(col + ub[b]) : 0ull;
-          c1b[b] = valid ? __ldg(col + ub[b] + 1) : 0ull;
+          c0b[b] = valid ? (ull)__ldg(col + ub[b]) : 0ull;
+          c1b[b] = valid ? (ull)__ldg(col + ub[b] + 1) : 0ull;
         }
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         const int b = y ? __ffs(y) - 1 : -1;
         y &= y ? y - 1 : 0u;
         const uint64_t u = w * 32 + (b < 0 ? 0 : b);
-        dd[q] = b < 0 ? 0ull : __ldg(col + u + 1) - __ldg(col + u);
+        dd[q] = b < 0 ? 0ull : (ull)(__ldg(col + u + 1) - __ldg(col + u));
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
       const int b = __ffs(y) - 1;
       y &= y - 1;
       const uint64_t u = w * 32 + b;
-      const ull c0 = __ldg(col + u), d = __ldg(col + u + 1) - c0;
+      const ull c0 = (ull)__ldg(col + u), d = (ull)__ldg(col + u + 1) - c0;
       if (d >= half) {
         const unsigned nt = (unsigned)((d + tm) >> tile_shift);
         emit_long(u, c0, d, aa, nt, hh);
@@ -584,13 +588,18 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   SegTot* st = static_cast<SegTot*>(rk.seg_tot);
   SegTot* ct = static_cast<SegTot*>(rk.seg_off);  // [grid] CTA totals, then [grid + 1] their scan
   SegTot* co = ct + grid;
-  k_scan_count<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts);
+  // narrow: the 32-bit copy of the column offsets (half the bytes of the col[] reads)
+  if (narrow) k_scan_count<uint32_t><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts);
+  else k_scan_count<ull><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts);
   // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
   k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
                                           kM3Factor, (ull)g.nrows());
-  auto emit = narrow ? k_scan_emit<true> : k_scan_emit<false>;
-  emit<<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff, rk.cumul,
-                                     rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
+  if (narrow)
+    k_scan_emit<true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, co, rk.flist, rk.rowoff,
+                                                    rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
+  else
+    k_scan_emit<false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff,
+                                                     rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
   k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
   return cudaGetLastError();
 }
@@ -1321,10 +1330,11 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
     return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
   };
   const uint64_t nchunks = (nwords + 31) / 32;
-  for (uint64_t ch = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid; ch < nchunks;
-       ch += (uint64_t)gridDim.x * (kParentThreads / 32)) {
-    const uint64_t w = ch * 32 + lane;
-    if (m3) {
+  const uint64_t cstride = (uint64_t)gridDim.x * (kParentThreads / 32);
+  const uint64_t first = (uint64_t)blockIdx.x * (kParentThreads / 32) + wid;
+  if (m3) {
+    for (uint64_t ch = first; ch < nchunks; ch += cstride) {
+      const uint64_t w = ch * 32 + lane;
       // mode 3: the rows claimed in pmin are the discovered ones; lane l handles row 32k + l of
       // the chunk's word k (coalesced), the ballot is word k's discovered bits
       uint32_t myd = 0;
@@ -1360,126 +1370,154 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
         }
       }
       ndisc += __popc(myd);
-      continue;
     }
-    const uint32_t d = (w < nwords) ? (vis[w] & ~vold[w]) : 0u;  // rows discovered in this level
-    if (sendbuf && w < nwords) sendbuf[w] = d;
-    if (fold_dst && w < nwords) {  // peer exchange (NVLink stores): segment c -> recv of P_ic
-      const uint64_t c = w / Wc;
-      if (fold_dst[c]) fold_dst[c][w - c * Wc] = d;
-    }
-    ndisc += __popc(d);
-    if (!__any_sync(0xFFFFFFFFu, d != 0)) continue;
-    if (p1) {
+  } else {
+    // P1 / P2: the chunk's rows discovered in this level (lane l: word ch*32 + l), their parents
+    auto process_chunk = [&](uint64_t w, uint32_t d) {
+      if (p1) {
+        uint32_t b = d;
+        while (b) {
+          const int bit = __ffs(b) - 1;
+          b &= b - 1;
+          const uint64_t r = w * 32 + bit;
+          put_pred(r, pmin[r]);
+          pmin[r] = 0xFFFFFFFFu;
+        }
+        return;
+      }
+      // exclusive prefix of popcounts across lanes -> queue positions
+      const unsigned c = __popc(d);
+      unsigned inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      unsigned pos = inc - c;
       uint32_t b = d;
       while (b) {
         const int bit = __ffs(b) - 1;
         b &= b - 1;
-        const uint64_t r = w * 32 + bit;
-        put_pred(r, pmin[r]);
-        pmin[r] = 0xFFFFFFFFu;
+        queue[wid][pos++] = (uint32_t)(w * 32 + bit);
       }
-      continue;
-    }
-    // exclusive prefix of popcounts across lanes -> queue positions
-    const unsigned c = __popc(d);
-    unsigned inc = c;
+      __syncwarp();
+      unsigned nlong = 0;  // lane-local count of deferred rows (written at slots lane, lane+32, ...)
+      // kParRows rows per lane at a time: their dependent chains (row pointers -> first CSR entries
+      // -> frontier tests -> inv_col) overlap, so more random loads are in flight per lane
+      for (unsigned q0 = lane; q0 < total; q0 += 32 * kParRows) {
+        uint32_t r[kParRows], best[kParRows];
+        ull p[kParRows], stop[kParRows];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const unsigned total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-    unsigned pos = inc - c;
-    uint32_t b = d;
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      queue[wid][pos++] = (uint32_t)(w * 32 + bit);
-    }
-    __syncwarp();
-    unsigned nlong = 0;  // lane-local count of deferred rows (written at slots lane, lane+32, ...)
-    // kParRows rows per lane at a time: their dependent chains (row pointers -> first CSR entries
-    // -> frontier tests -> inv_col) overlap, so more random loads are in flight per lane
-    for (unsigned q0 = lane; q0 < total; q0 += 32 * kParRows) {
-      uint32_t r[kParRows], best[kParRows];
-      ull p[kParRows], stop[kParRows];
-#pragma unroll
-      for (int i = 0; i < kParRows; ++i) r[i] = (q0 + 32 * i < total) ? queue[wid][q0 + 32 * i] : 0xFFFFFFFFu;
-#pragma unroll
-      for (int i = 0; i < kParRows; ++i) {
-        const bool v = r[i] != 0xFFFFFFFFu;
-        const ull beg = v ? csr_ptr[r[i]] : 0ull, end = v ? csr_ptr[r[i] + 1] : 0ull;
-        p[i] = beg;
-        stop[i] = min(end, beg + kShortScan);
-        best[i] = 0xFFFFFFFFu;
-      }
-      bool more = true;
-      while (more) {  // every row still searching takes one lane step, all rows' loads together
-        uint32_t u[kParRows][kLaneStep];
+        for (int i = 0; i < kParRows; ++i) r[i] = (q0 + 32 * i < total) ? queue[wid][q0 + 32 * i] : 0xFFFFFFFFu;
 #pragma unroll
         for (int i = 0; i < kParRows; ++i) {
-          const bool act = best[i] == 0xFFFFFFFFu && p[i] < stop[i];
-#pragma unroll
-          for (int k = 0; k < kLaneStep; ++k)
-            u[i][k] = (act && p[i] + k < stop[i]) ? __ldg(csr_col + p[i] + k) : 0xFFFFFFFFu;
+          const bool v = r[i] != 0xFFFFFFFFu;
+          const ull beg = v ? csr_ptr[r[i]] : 0ull, end = v ? csr_ptr[r[i] + 1] : 0ull;
+          p[i] = beg;
+          stop[i] = min(end, beg + kShortScan);
+          best[i] = 0xFFFFFFFFu;
         }
-        more = false;
+        bool more = true;
+        while (more) {  // every row still searching takes one lane step, all rows' loads together
+          uint32_t u[kParRows][kLaneStep];
 #pragma unroll
-        for (int i = 0; i < kParRows; ++i) {
-          bool f[kLaneStep];
+          for (int i = 0; i < kParRows; ++i) {
+            const bool act = best[i] == 0xFFFFFFFFu && p[i] < stop[i];
 #pragma unroll
-          for (int k = 0; k < kLaneStep; ++k) f[k] = (u[i][k] != 0xFFFFFFFFu) && in_front(u[i][k]);
+            for (int k = 0; k < kLaneStep; ++k)
+              u[i][k] = (act && p[i] + k < stop[i]) ? __ldg(csr_col + p[i] + k) : 0xFFFFFFFFu;
+          }
+          more = false;
 #pragma unroll
-          for (int k = kLaneStep - 1; k >= 0; --k)
-            if (f[k]) best[i] = u[i][k];
-          p[i] += kLaneStep;
-          more |= best[i] == 0xFFFFFFFFu && p[i] < stop[i];
-        }
-      }
-      uint32_t pv[kParRows];
+          for (int i = 0; i < kParRows; ++i) {
+            bool f[kLaneStep];
 #pragma unroll
-      for (int i = 0; i < kParRows; ++i)
-        pv[i] = (r[i] != 0xFFFFFFFFu && best[i] != 0xFFFFFFFFu) ? inv_col[best[i]] : 0u;
+            for (int k = 0; k < kLaneStep; ++k) f[k] = (u[i][k] != 0xFFFFFFFFu) && in_front(u[i][k]);
 #pragma unroll
-      for (int i = 0; i < kParRows; ++i) {
-        if (r[i] == 0xFFFFFFFFu) continue;
-        BCHECK(r[i] < nwords * 32 && (best[i] == 0xFFFFFFFFu || best[i] < info->cap_ncols));
-        if (best[i] != 0xFFFFFFFFu) {
-          put_pred(r[i], pv[i]);
-        } else {  // defer to the whole warp; slot lane+32*nlong <= q0+32i was already read
-          queue[wid][lane + 32 * nlong] = r[i];
-          ++nlong;
-        }
-      }
-    }
-    __syncwarp();
-    // cooperative scan of the deferred rows: lane l's k-th row sits at slot l + 32k
-    unsigned maxlong = nlong;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) maxlong = max(maxlong, __shfl_xor_sync(0xFFFFFFFFu, maxlong, o));
-    for (unsigned k = 0; k < maxlong; ++k) {
-      unsigned has = __ballot_sync(0xFFFFFFFFu, k < nlong);
-      while (has) {
-        const int src = __ffs(has) - 1;
-        has &= has - 1;
-        const uint32_t r = queue[wid][src + 32 * k];
-        const ull end = csr_ptr[r + 1];
-        uint32_t best = 0xFFFFFFFFu;
-        for (ull p = csr_ptr[r] + kShortScan; p < end; p += 32) {
-          const uint32_t u = (p + lane < end) ? __ldg(csr_col + p + lane) : 0xFFFFFFFFu;
-          const bool f = (u != 0xFFFFFFFFu) && in_front(u);
-          const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
-          if (m) {
-            best = __shfl_sync(0xFFFFFFFFu, u, __ffs(m) - 1);
-            break;
+            for (int k = kLaneStep - 1; k >= 0; --k)
+              if (f[k]) best[i] = u[i][k];
+            p[i] += kLaneStep;
+            more |= best[i] == 0xFFFFFFFFu && p[i] < stop[i];
           }
         }
-        BCHECK(best < info->cap_ncols);  // a discovered row has a frontier neighbour in its CSR row
-        if (lane == 0) put_pred(r, inv_col[best]);
+        uint32_t pv[kParRows];
+#pragma unroll
+        for (int i = 0; i < kParRows; ++i)
+          pv[i] = (r[i] != 0xFFFFFFFFu && best[i] != 0xFFFFFFFFu) ? inv_col[best[i]] : 0u;
+#pragma unroll
+        for (int i = 0; i < kParRows; ++i) {
+          if (r[i] == 0xFFFFFFFFu) continue;
+          BCHECK(r[i] < nwords * 32 && (best[i] == 0xFFFFFFFFu || best[i] < info->cap_ncols));
+          if (best[i] != 0xFFFFFFFFu) {
+            put_pred(r[i], pv[i]);
+          } else {  // defer to the whole warp; slot lane+32*nlong <= q0+32i was already read
+            queue[wid][lane + 32 * nlong] = r[i];
+            ++nlong;
+          }
+        }
+      }
+      __syncwarp();
+      // cooperative scan of the deferred rows: lane l's k-th row sits at slot l + 32k
+      unsigned maxlong = nlong;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) maxlong = max(maxlong, __shfl_xor_sync(0xFFFFFFFFu, maxlong, o));
+      for (unsigned k = 0; k < maxlong; ++k) {
+        unsigned has = __ballot_sync(0xFFFFFFFFu, k < nlong);
+        while (has) {
+          const int src = __ffs(has) - 1;
+          has &= has - 1;
+          const uint32_t r = queue[wid][src + 32 * k];
+          const ull end = csr_ptr[r + 1];
+          uint32_t best = 0xFFFFFFFFu;
+          for (ull p = csr_ptr[r] + kShortScan; p < end; p += 32) {
+            const uint32_t u = (p + lane < end) ? __ldg(csr_col + p + lane) : 0xFFFFFFFFu;
+            const bool f = (u != 0xFFFFFFFFu) && in_front(u);
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
+            if (m) {
+              best = __shfl_sync(0xFFFFFFFFu, u, __ffs(m) - 1);
+              break;
+            }
+          }
+          BCHECK(best < info->cap_ncols);  // a discovered row has a frontier neighbour in its CSR row
+          if (lane == 0) put_pred(r, inv_col[best]);
+        }
+      }
+      __syncwarp();
+    };
+    // Chunks in groups of 32 per warp: pass 1 loads the discovered words of the group (8 chunks'
+    // loads in flight), writes the fold message and marks the non-empty chunks; pass 2 runs the
+    // parent claims of those only -- sparse levels end after pass 1's round trips.
+    for (uint64_t g0 = first; g0 < nchunks; g0 += 32 * cstride) {
+      unsigned mask = 0;
+      for (int q0 = 0; q0 < 32; q0 += 8) {
+        uint32_t dv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t ch = g0 + (uint64_t)(q0 + q) * cstride, w = ch * 32 + lane;
+          dv[q] = (ch < nchunks && w < nwords) ? (vis[w] & ~vold[w]) : 0u;  // rows discovered in this level
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t ch = g0 + (uint64_t)(q0 + q) * cstride, w = ch * 32 + lane;
+          if (ch >= nchunks) break;  // warp-uniform
+          const uint32_t d = dv[q];
+          if (sendbuf && w < nwords) sendbuf[w] = d;
+          if (fold_dst && w < nwords) {  // peer exchange (NVLink stores): segment c -> recv of P_ic
+            const uint64_t c = w / Wc;
+            if (fold_dst[c]) fold_dst[c][w - c * Wc] = d;
+          }
+          ndisc += __popc(d);
+          if (__any_sync(0xFFFFFFFFu, d != 0)) mask |= 1u << (q0 + q);
+        }
+      }
+      while (mask) {
+        const int q = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint64_t ch = g0 + (uint64_t)q * cstride, w = ch * 32 + lane;
+        process_chunk(w, (w < nwords) ? (vis[w] & ~vold[w]) : 0u);
       }
     }
-    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) ndisc += __shfl_xor_sync(0xFFFFFFFFu, ndisc, o);
@@ -1531,68 +1569,83 @@ cudaError_t kernels_init_device() {
 // rows received from any column (own discoveries included) that are not yet visited; the
 // lowest sending column is recorded as the parent's column (winner).  Other segments: mark the
 // rows this rank discovered as visited so they are sent at most once.
+constexpr int kUpdWords = 4;  // words per thread of K2 (their loads in flight together)
 __global__ void __launch_bounds__(256) k_update(uint32_t* vis, uint32_t* vold, const uint32_t* recv,
                                                 uint32_t* front_seg,
                                                 int32_t* level, uint8_t* winner, LevelInfo* info, uint64_t W, int C,
                                                 int j, const LevelCtrl* ctrl, uint32_t* const* __restrict__ exp_dst,
                                                 int R) {
-  // grid: x strides over the words of one segment (one pass unless the grid is capped), y = segment m
+  // grid: x strides over the words of one segment (kUpdWords groups of 256 words per CTA and
+  // step), y = segment m
   const int lvl = (int)ctrl->lvl;  // the level being assigned (device-side: the loop may be a graph)
   const int m = (int)blockIdx.y;
   const int lane = threadIdx.x & 31;
   unsigned cnt = 0;
-  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x; wb < W; wb += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t w = wb + threadIdx.x;
-    const uint64_t gid = (uint64_t)m * W + w;
-    uint32_t newbits = 0;
-    uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
-    if (m == j && w < W) {
-      const uint32_t vo = vold[gid], own = vis[gid] & ~vo;  // level-start bits, own discoveries
-      uint32_t claimed = 0;
-      for (int c = 0; c < C; ++c) {
-        const uint32_t x = ((c == j) ? own : recv[(uint64_t)c * W + w]) & ~vo & ~claimed;
-        if (c < 8) wbits[c] = x;
-        if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
-          uint32_t b = x;
-          while (b) {
-            const int bit = __ffs(b) - 1;
-            b &= b - 1;
-            winner[w * 32 + bit] = (uint8_t)c;
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * kUpdWords;
+  for (uint64_t wb0 = (uint64_t)blockIdx.x * blockDim.x * kUpdWords; wb0 < W; wb0 += step) {
+    uint32_t vo[kUpdWords], vn[kUpdWords];
+#pragma unroll
+    for (int q = 0; q < kUpdWords; ++q) {  // all the thread's words in one round trip
+      const uint64_t w = wb0 + (uint64_t)q * blockDim.x + threadIdx.x;
+      const uint64_t gid = (uint64_t)m * W + w;
+      vo[q] = w < W ? vold[gid] : 0u;
+      vn[q] = w < W ? vis[gid] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kUpdWords; ++q) {
+      const uint64_t wb = wb0 + (uint64_t)q * blockDim.x;
+      if (wb >= W) break;  // CTA-uniform
+      const uint64_t w = wb + threadIdx.x;
+      const uint64_t gid = (uint64_t)m * W + w;
+      uint32_t newbits = 0;
+      uint32_t wbits[8];  // winner column c's share of newbits (C <= 8 per row of the grid is typical)
+      if (m == j && w < W) {
+        const uint32_t own = vn[q] & ~vo[q];  // own discoveries (vo: the level-start bits)
+        uint32_t claimed = 0;
+        for (int c = 0; c < C; ++c) {
+          const uint32_t x = ((c == j) ? own : recv[(uint64_t)c * W + w]) & ~vo[q] & ~claimed;
+          if (c < 8) wbits[c] = x;
+          if (x && winner && c >= 8) {  // wide grids: per-bit winner stores
+            uint32_t b = x;
+            while (b) {
+              const int bit = __ffs(b) - 1;
+              b &= b - 1;
+              winner[w * 32 + bit] = (uint8_t)c;
+            }
+          }
+          claimed |= x;
+        }
+        newbits = claimed;  // includes own (own discoveries were not visited at the level start)
+        if (newbits) vis[gid] = vold[gid] = vo[q] | newbits;
+        front_seg[w] = newbits;
+        if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
+          for (int i2 = 0; i2 < R; ++i2)
+            if (exp_dst[i2]) exp_dst[i2][w] = newbits;
+      } else if (w < W) {  // rows of other owners discovered here stay visited on this rank
+        if (vn[q] != vo[q]) vold[gid] = vn[q];
+      }
+      // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing
+      // vertex 32k + l of word k (coalesced stores instead of per-bit scattered ones)
+      if (m == j) {
+        const uint64_t wbase = w - lane;
+        unsigned nz = __ballot_sync(0xFFFFFFFFu, newbits != 0);
+        while (nz) {
+          const int k = __ffs(nz) - 1;
+          nz &= nz - 1;
+          const uint32_t nb = __shfl_sync(0xFFFFFFFFu, newbits, k);
+          const uint64_t v = (wbase + k) * 32 + lane;
+          if ((nb >> lane) & 1u) level[v] = lvl;
+          if (winner) {
+            const int cmax = C < 8 ? C : 8;
+            for (int c = 0; c < cmax; ++c) {
+              const uint32_t x = __shfl_sync(0xFFFFFFFFu, wbits[c], k);
+              if ((x >> lane) & 1u) winner[v] = (uint8_t)c;
+            }
           }
         }
-        claimed |= x;
       }
-      newbits = claimed;  // includes own (own discoveries were not visited at the level start)
-      if (newbits) vis[gid] = vold[gid] = vo | newbits;
-      front_seg[w] = newbits;
-      if (exp_dst)  // peer exchange (NVLink stores): the next frontier segment into the column peers
-        for (int i2 = 0; i2 < R; ++i2)
-          if (exp_dst[i2]) exp_dst[i2][w] = newbits;
-    } else if (w < W) {  // rows of other owners discovered here stay visited on this rank
-      const uint32_t vn = vis[gid];
-      if (vn != vold[gid]) vold[gid] = vn;
+      cnt += __popc(newbits);
     }
-    // levels (and winners) of the new vertices: the warp walks its 32 words, lane l writing vertex
-    // 32k + l of word k (coalesced stores instead of per-bit scattered ones)
-    if (m == j) {
-      const uint64_t wbase = w - lane;
-      unsigned nz = __ballot_sync(0xFFFFFFFFu, newbits != 0);
-      while (nz) {
-        const int k = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t nb = __shfl_sync(0xFFFFFFFFu, newbits, k);
-        const uint64_t v = (wbase + k) * 32 + lane;
-        if ((nb >> lane) & 1u) level[v] = lvl;
-        if (winner) {
-          const int cmax = C < 8 ? C : 8;
-          for (int c = 0; c < cmax; ++c) {
-            const uint32_t x = __shfl_sync(0xFFFFFFFFu, wbits[c], k);
-            if ((x >> lane) & 1u) winner[v] = (uint8_t)c;
-          }
-        }
-      }
-    }
-    cnt += __popc(newbits);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
@@ -1605,7 +1658,7 @@ __global__ void __launch_bounds__(256) k_update(uint32_t* vis, uint32_t* vold, c
 
 cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s) {
   const uint64_t W = g.words_block();
-  uint64_t gx = (W + 255) / 256;
+  uint64_t gx = (W + 256 * kUpdWords - 1) / (256 * kUpdWords);
   // peer stores: each CTA ends with a system-scope fence, so a capped grid strides instead
   const uint64_t cap = (uint64_t)g.nsm * 8 / (uint64_t)g.C;
   if (g.R > 1 && rk.exp_dst && gx > cap) gx = cap ? cap : 1;
