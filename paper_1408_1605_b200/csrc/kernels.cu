@@ -29,6 +29,11 @@ namespace bfs200 {
 
 typedef unsigned long long ull;
 
+// row slots of the pipelined long-tile loop of K1 (long_tiles_p2; 0 = the double-buffered loop)
+#ifndef BFS200_K1PIPE
+#define BFS200_K1PIPE 3
+#endif
+
 // ------------------------------------------------------------------ small helpers
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t v;
@@ -396,13 +401,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   unsigned nlongcols = 0;
   __shared__ uint16_t s_lists[kScanThreads / 32][1024];
   uint16_t* s_list = s_lists[threadIdx.x >> 5];
+  // compact 8-byte long-tile records (position, length) in P2 levels of the pipelined loop (the
+  // column is only needed by the P1 claims): half the record traffic of K3 and K1
+  const bool compact = NARROW && BFS200_K1PIPE > 0 && info->mode == 2 && tile_shift <= 8;
   auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt, uint64_t hub) {
     if (nt <= 8) {
       for (unsigned q = 0; q < nt; ++q) {
         const ull pos = c0 + ((ull)q << tile_shift);
         const ull len = min(d - ((ull)q << tile_shift), tm + 1);
         BCHECK(pa + q < info->cap_tiles && pos + len <= info->cap_nnz);
-        tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
+        if (compact) reinterpret_cast<uint2*>(tileA)[pa + q] = make_uint2((uint32_t)pos, (uint32_t)len);
+        else tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
       }
     } else {  // hub column: its tiles are written by k_tile_fill
       BCHECK(2 * hub + 1 < info->cap_long && c0 + d <= info->cap_nnz);
@@ -563,8 +572,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
 }
 
 // long-tile records of hub columns: one warp per column
-__global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4* tileA, int tile_shift) {
+__global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4* tileA, int tile_shift, int narrow) {
   const int lane = threadIdx.x & 31;
+  const bool compact = narrow && BFS200_K1PIPE > 0 && info->mode == 2 && tile_shift <= 8;  // as in k_scan_emit
   const ull nl = info->nlong;
   const ull tm = (1ull << tile_shift) - 1;
   for (ull r = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nl; r += ((ull)gridDim.x * blockDim.x) >> 5) {
@@ -575,7 +585,8 @@ __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4*
       const ull pos = c0 + ((ull)q << tile_shift);
       const ull len = min(d - ((ull)q << tile_shift), tm + 1);
       BCHECK(pa + q < info->cap_tiles && pos + len <= info->cap_nnz);
-      tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, h.z);
+      if (compact) reinterpret_cast<uint2*>(tileA)[pa + q] = make_uint2((uint32_t)pos, (uint32_t)len);
+      else tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, h.z);
     }
   }
 }
@@ -600,7 +611,7 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   else
     k_scan_emit<false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff,
                                                      rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
-  k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts);
+  k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts, narrow ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -772,9 +783,6 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 // spills); the REDs deferred one phase behind the next tile's probes: 3.34 ms (NS = 2); a
 // warp-uniform full-tile branch without per-lane bounds: 3.46 ms; a probe returning x = ~0 instead
 // of a need flag: 3.17 ms.
-#ifndef BFS200_K1PIPE
-#define BFS200_K1PIPE 3
-#endif
 // Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
 // keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
 // word address from v (two instructions instead of three live registers per row).
@@ -852,10 +860,17 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
     rlen[slot] = 0u;
     rpos[slot] = 0;
     if (t < nA) {
-      const uint4 r = tileA[t];
-      BCHECK(((ull)r.x | ((ull)r.y << 32)) + r.z <= info->cap_nnz && r.z <= 32u * E);
-      rpos[slot] = POS32 ? (Pos)r.x : (Pos)((ull)r.x | ((ull)r.y << 32));
-      rlen[slot] = r.z;
+      if (POS32) {  // compact records (k_scan_emit: narrow, P2, E <= 8)
+        const uint2 r = reinterpret_cast<const uint2*>(tileA)[t];
+        BCHECK((ull)r.x + r.y <= info->cap_nnz && r.y <= 32u * E);
+        rpos[slot] = (Pos)r.x;
+        rlen[slot] = r.y;
+      } else {
+        const uint4 r = tileA[t];
+        BCHECK(((ull)r.x | ((ull)r.y << 32)) + r.z <= info->cap_nnz && r.z <= 32u * E);
+        rpos[slot] = (Pos)((ull)r.x | ((ull)r.y << 32));
+        rlen[slot] = r.z;
+      }
     }
   };
   auto rows_issue = [&](int slot) {  // from the record in the same slot
