@@ -207,6 +207,8 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
   AL(rk.seg_tot, (nseg + 1) * 32);
   AL(rk.seg_off, (nseg + 8) * 32);  // CTA totals (nseg/8 + 1) and their scan (nseg/8 + 2)
+  AL(rk.scan_ticket, 16);
+  CKR(cudaMemsetAsync(rk.scan_ticket, 0, 16, G.stream));
   CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
@@ -770,6 +772,10 @@ static int resolve_parents(Graph& G) {
 // captured into the body of the CUDA-graph WHILE node (no phase events then).
 // 32-bit K3/K1 offsets when every CSC position of the rank fits (the same test as K1's POS32
 // variant; the test-only BFS_DEBUG_POS64 flag forces the 64-bit path in both)
+// 1x1 graph with the level loop on one stream: K2's frontier update moves into the next level's
+// count pass (kernels.cu FusedUpd) and K4 counts the new vertices
+static bool fused_of(const Graph& G) { return G.g.R == 1 && G.g.C == 1 && G.ranks.size() == 1; }
+
 static bool narrow_of(const Graph& G, const Rank& rk) {
   return rk.nnz < (1ull << 32) && !(G.opts.debug_flags & BFS_DEBUG_POS64);
 }
@@ -787,11 +793,11 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
     Rank& rk = G.ranks[0];
     if (ev && (rc = ev_rec(G, nlev, 0))) return rc;
     if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
-    CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), s));
+    CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), fused_of(G) ? G.d_ctrl : nullptr, s));
     if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
     CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
     if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
-    CKR(launch_parent(g, rk, s));
+    CKR(launch_parent(g, rk, fused_of(G), s));
     if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
     // barrier 1: every fold store has landed, and every rank is done reading its frontier bitmap
     // (K2's peer stores below overwrite it)
@@ -808,15 +814,16 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   const bool xl = G.opts.exchange != BFS_XCHG_BITMAP;  // never inside a graph capture
   if ((rc = xl ? expand_exchange_x(G) : expand_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 1))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), s));
+  for (Rank& rk : G.ranks) CKR(launch_scan(g, rk, tile_edges, narrow_of(G, rk), fused_of(G) ? G.d_ctrl : nullptr, s));
   if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
   if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, s));
+  for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, fused_of(G), s));
   if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
   if ((rc = xl ? fold_exchange_x(G) : fold_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 5))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_update(g, rk, G.d_ctrl, s));
+  if (!fused_of(G))
+    for (Rank& rk : G.ranks) CKR(launch_update(g, rk, G.d_ctrl, s));
   if (ev && (rc = ev_rec(G, nlev, 6))) return rc;
   if (G.world_size > 1) NKR(ncclAllReduce(&G.infos[0].newv, &G.infos[0].newv, 1, ncclUint64, ncclSum, G.world, s));
   CKR(launch_level_end(G.d_ctrl, G.infos, (int)G.ranks.size(), G.world_size > 1, G.cond, use_cond, s));
@@ -875,7 +882,7 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   }
   for (Rank& rk : G.ranks) {
     owner_local |= (uint64_t)rk.r == owner;
-    CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, s));
+    CKR(launch_init(g, rk, (uint64_t)rk.r == owner, root, fused_of(G), s));
     // peer exchange: no all-gather before level 1, so the owner's column peers seed the bit
     const int owner_i = (int)(owner % (uint64_t)g.R), owner_j = (int)(owner / (uint64_t)g.R);
     if (peer_active(G) && (uint64_t)rk.r != owner && rk.j == owner_j)
@@ -996,13 +1003,13 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
     stats->reached = 0;
     // own kernels: seed (owner only), level_begin, per level level_end and per local rank
-    // scan(4) + expand + parent + update, then finalize; with C > 1 the resolution adds
+    // scan(3) + expand + parent + update (no update on a fused 1x1 graph), then finalize; with C > 1 the resolution adds
     // req_build, 2 seg_totals and resp_pack.
     const uint64_t nl = G.ranks.size();
     const bool peer = peer_active(G);
     const int owner_j = (int)(owner / (uint64_t)g.R);
     stats->kernel_launches =
-        (owner_local ? 1 : 0) + 1 + nlev + nl * (7ull * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
+        (owner_local ? 1 : 0) + 1 + nlev + nl * ((fused_of(G) ? 5ull : 6ull) * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
         G.xlaunches +
         (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
   }

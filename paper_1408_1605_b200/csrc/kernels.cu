@@ -92,11 +92,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ------------------------------------------------------------------ init (Alg.2 lines 1-10)
 __global__ void k_seed_root(uint32_t* vis, uint32_t* vold, uint32_t* all_front, int32_t* level, uint32_t* pred, uint8_t* winner,
+                            int fused,
                             const uint32_t* fwd_own, uint64_t t0, uint64_t block, int i, uint32_t root, int j) {
   const uint64_t t = fwd_own[t0];  // relabeled offset of the root in its block
   const uint64_t row_local = (uint64_t)j * block + t, col_local = (uint64_t)i * block + t;
   vis[row_local >> 5] |= 1u << (row_local & 31);   // bmap[LOCAL_ROW(r)] <- 1
-  vold[row_local >> 5] |= 1u << (row_local & 31);
+  if (!fused) vold[row_local >> 5] |= 1u << (row_local & 31);  // fused: level 1's count pass takes it
   all_front[col_local >> 5] |= 1u << (col_local & 31);  // front[0] <- LOCAL_COL(r)
   level[t] = 0;                                          // level[LOCAL_ROW(r)] <- 0
   pred[row_local] = root;                                // pred[LOCAL_ROW(r)] <- r
@@ -105,7 +106,7 @@ __global__ void k_seed_root(uint32_t* vis, uint32_t* vold, uint32_t* all_front, 
 
 // level[] and pred[] need no reset: both are written for a vertex when it is reached, and every
 // reader masks with the visited bit (unreached -> -1).
-cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s) {
+cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, bool fused, cudaStream_t s) {
   const uint64_t rw = g.nrows() / 32, cw = g.ncols() / 32;
   cudaError_t e = cudaMemsetAsync(rk.vis, 0, rw * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(rk.vold, 0, rw * 4, s);
@@ -114,7 +115,7 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cuda
   if (e != cudaSuccess) return e;
   if (owner) {
     const uint64_t t = root - (uint64_t)rk.r * g.block;
-    k_seed_root<<<1, 1, 0, s>>>(rk.vis, rk.vold, rk.all_front, rk.level, rk.pred, rk.winner, rk.fwd_own, t, g.block, rk.i,
+    k_seed_root<<<1, 1, 0, s>>>(rk.vis, rk.vold, rk.all_front, rk.level, rk.pred, rk.winner, fused ? 1 : 0, rk.fwd_own, t, g.block, rk.i,
                                 (uint32_t)root, rk.j);
   }
   return cudaGetLastError();
@@ -140,22 +141,185 @@ struct SegTot {
   ull ls;           // long edges
 };
 static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
+#ifndef BFS200_BLIND3
+#define BFS200_BLIND3 1
+#endif
+constexpr bool kBlind3 = BFS200_BLIND3;
+
+// Parent-claim mode thresholds (level_bookkeeping; measured at s26): P2 when a row's
+// expected CSR scan is <= kP2Factor entries; mode 3 when the P1 candidate edges are >= rows / kM3Factor.
+constexpr ull kP2Factor = 8;
+constexpr ull kM3Factor = 4;
+
+// K3 scan of the per-CTA totals of the count pass, fused into that pass: the last CTA to finish
+// (an atomic ticket after each CTA's totals are written and fenced) scans the CTA totals --
+// each thread sums up to kScanItems consecutive totals, one block scan of the thread sums, the
+// exclusive prefixes written back (seg_off[n] = the level's totals) -- and does the level
+// bookkeeping (counts, parent-claim mode).  No separate launch, no library scan.
+constexpr int kScanItems = 8;
+struct SegAcc {  // the scanned fields (pad is never summed)
+  unsigned cs, na, nh;
+  ull ss, ls;
+};
+__device__ __forceinline__ SegAcc seg_add(const SegAcc& a, const SegAcc& b) {
+  return SegAcc{a.cs + b.cs, a.na + b.na, a.nh + b.nh, a.ss + b.ss, a.ls + b.ls};
+}
+__device__ __forceinline__ SegAcc seg_sub(const SegAcc& a, const SegAcc& b) {
+  return SegAcc{a.cs - b.cs, a.na - b.na, a.nh - b.nh, a.ss - b.ss, a.ls - b.ls};
+}
+__device__ __forceinline__ SegAcc seg_shfl_up(const SegAcc& a, int d) {
+  return SegAcc{__shfl_up_sync(0xFFFFFFFFu, a.cs, d), __shfl_up_sync(0xFFFFFFFFu, a.na, d),
+                __shfl_up_sync(0xFFFFFFFFu, a.nh, d), __shfl_up_sync(0xFFFFFFFFu, a.ss, d),
+                __shfl_up_sync(0xFFFFFFFFu, a.ls, d)};
+}
+// (L2 loads: the totals were written by other CTAs of the same kernel)
+__device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t n) {
+  if (k >= n) return SegAcc{0u, 0u, 0u, 0ull, 0ull};
+  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p + k);
+  const ulonglong2 a = __ldcg(q), b = __ldcg(q + 1);  // {cs | na << 32, nh | pad << 32}, {ss, ls}
+  return SegAcc{(unsigned)a.x, (unsigned)(a.x >> 32), (unsigned)a.y, b.x, b.y};
+}
+
+
+// exclusive scan of tot[0..n) into off[0..n], by the NT threads of one CTA; returns the total
+template <int NT>
+__device__ __forceinline__ SegAcc block_scan_totals(const SegTot* tot, uint64_t n, SegTot* off, SegAcc* s_warp) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  SegAcc carry{0u, 0u, 0u, 0ull, 0ull};
+  for (uint64_t base = 0; base < n; base += (uint64_t)NT * kScanItems) {
+    const uint64_t k0 = base + (uint64_t)threadIdx.x * kScanItems;
+    SegAcc v[kScanItems];
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) v[q] = seg_load(tot, k0 + q, n);  // all in flight
+    SegAcc mine{0u, 0u, 0u, 0ull, 0ull};
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) mine = seg_add(mine, v[q]);
+    SegAcc inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const SegAcc y = seg_shfl_up(inc, d);
+      if (lane >= d) inc = seg_add(inc, y);
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const SegAcc w = lane < NT / 32 ? s_warp[lane] : SegAcc{0u, 0u, 0u, 0ull, 0ull};
+      SegAcc wi = w;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const SegAcc y = seg_shfl_up(wi, d);
+        if (lane >= d) wi = seg_add(wi, y);
+      }
+      if (lane < NT / 32) s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
+      if (lane == 31) s_warp[NT / 32] = wi;               // the pass total
+    }
+    __syncthreads();
+    SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, mine)));
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) {
+      if (k0 + q < n) off[k0 + q] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
+      ex = seg_add(ex, v[q]);
+    }
+    carry = seg_add(carry, s_warp[NT / 32]);
+    __syncthreads();  // s_warp is rewritten by the next pass
+  }
+  return carry;
+}
+
+// the level's totals and bookkeeping (one thread)
+struct LevelParams {
+  void* cumul;
+  int narrow;
+  ull nnz, p2_factor, nz_rows, m3_factor, nrows;
+};
+__device__ __forceinline__ void level_bookkeeping(const SegAcc& c, uint64_t n, SegTot* seg_off, LevelInfo* info,
+                                                  const LevelParams& lp) {
+  const ull nnz = lp.nnz, p2_factor = lp.p2_factor, nz_rows = lp.nz_rows, m3_factor = lp.m3_factor,
+            nrows = lp.nrows;
+  void* cumul = lp.cumul;
+  const int narrow = lp.narrow;
+  seg_off[n] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
+  // level totals; resets the per-level counters
+  info->n = c.cs;
+  info->sedges = c.ss;
+  info->nA = c.na;
+  info->edges = c.ss + c.ls;
+  info->ncols = c.cs;
+  info->newv = 0;
+  // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
+  // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
+  // the scan (P2) is used when that is <= p2_factor (default 8); otherwise (small frontiers,
+  // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).  P2 also when
+  // few rows remain to be discovered (the scans are then few, whatever their length):
+  // remaining = rows with entries - rows discovered so far (an estimate on this rank).
+  const ull edges = c.ss + c.ls, seen = info->disc_total;
+  const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
+  info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
+  // P1 with many candidate edges (mode 3): the expansion only claims (atomicMin); the parent
+  // pass derives the discovered words from pmin in one pass over the rows (cheaper than a
+  // RED.OR and a probe per edge once edges * m3_factor >= rows)
+  if (info->mode == 1 && m3_factor && edges * m3_factor >= nrows) info->mode = 3ull;
+  // mode 3 while at most 1/16 of the rows are visited (the first dense level): the visited
+  // probe of a non-hot row almost never finds the bit set, so the claim goes out without it
+  info->blind = (info->mode == 3 && kBlind3 && seen * 16ull <= nz_rows) ? 1ull : 0ull;
+  info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
+  info->nlongcols = 0;
+  if (narrow) static_cast<uint32_t*>(cumul)[c.cs] = (uint32_t)c.ss;
+  else static_cast<ull*>(cumul)[c.cs] = c.ss;
+}
+
 // Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
 // chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
-template <typename Col>
+// Fused frontier update of a 1x1 graph (no exchange between K4 and K3): K2 does not run; the
+// count pass of the NEXT level takes the frontier as the rows discovered in the previous level,
+// f = vis & ~vold, writes it to the frontier bitmap (read by the emit pass and K4), advances
+// vold and writes the rows' level (ctrl->lvl - 1).  The root is seeded into vis only.
+struct FusedUpd {
+  const uint32_t* vis;
+  uint32_t* vold;
+  uint32_t* front;  // the frontier bitmap written here (== the bm the emit pass reads)
+  int32_t* level;
+  const LevelCtrl* ctrl;
+};
+
+template <typename Col, bool FUSED>
 __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uint64_t nwords, uint64_t seg,
-                                            const Col* __restrict__ col, int tile_shift) {
+                                            const Col* __restrict__ col, int tile_shift, const FusedUpd& fu) {
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
   const ull half = 1ull << (tile_shift - 1), tm = (1ull << tile_shift) - 1;
   SegTot t{0u, 0u, 0ull, 0ull};
+  uint32_t xw[kScanSegWords / 32];  // the segment's words, lane l: word w0 + 32c + l
   {  // all words of the segment in one round trip; an empty segment (sparse levels) ends here
     uint32_t any = 0;
 #pragma unroll
     for (int c = 0; c < kScanSegWords / 32; ++c) {
       const uint64_t w = w0 + 32 * c + lane;
-      any |= (w < w1) ? __ldg(bm + w) : 0u;
+      if (FUSED) {
+        const uint32_t vn = (w < w1) ? fu.vis[w] : 0u, vo = (w < w1) ? fu.vold[w] : 0u;
+        xw[c] = vn & ~vo;
+        if (w < w1) {
+          fu.front[w] = xw[c];
+          if (xw[c]) fu.vold[w] = vn;
+        }
+      } else {
+        xw[c] = (w < w1) ? __ldg(bm + w) : 0u;
+      }
+      any |= xw[c];
+    }
+    if (FUSED) {  // levels of the new frontier, lane l writing vertex 32k + l of word k (coalesced)
+      const int32_t lv = (int32_t)fu.ctrl->lvl - 1;
+#pragma unroll
+      for (int c = 0; c < kScanSegWords / 32; ++c) {
+        unsigned nz = __ballot_sync(0xFFFFFFFFu, xw[c] != 0u);
+        while (nz) {
+          const int k = __ffs(nz) - 1;
+          nz &= nz - 1;
+          const uint32_t nb = __shfl_sync(0xFFFFFFFFu, xw[c], k);
+          if ((nb >> lane) & 1u) fu.level[(w0 + 32 * c + k) * 32 + lane] = lv;
+        }
+      }
     }
     if (!__any_sync(0xFFFFFFFFu, any != 0u)) return SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
   }
@@ -172,9 +336,15 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
       t.ss += d;
     }
   };
-  for (uint64_t wb = w0; wb < w1; wb += 32) {
+#pragma unroll 1
+  for (int cw = 0; cw < kScanSegWords / 32; ++cw) {
+    const uint64_t wb = w0 + 32 * cw;
+    if (wb >= w1) break;  // warp-uniform
     const uint64_t w = wb + lane;
-    uint32_t x = (w < w1) ? __ldg(bm + w) : 0u;
+    uint32_t x = xw[0];  // xw[cw] without dynamic indexing (stays in registers)
+#pragma unroll
+    for (int c = 1; c < kScanSegWords / 32; ++c)
+      if (cw == c) x = xw[c];
     const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
     if (nbits >= 96) {
       // dense chunk: compact the set bits, then 32 consecutive frontier columns per step (their
@@ -228,136 +398,43 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
 }
 
 // Per-segment totals (seg_tot[seg]) and per-CTA totals of the kScanThreads/32 segments of a CTA
-// (cta_tot[b]): the single-CTA scan (k_seg_scan) then only scans the few CTA totals, and the
+// (cta_tot[b]): the last CTA then scans only the few CTA totals (block_scan_totals), and the
 // emit pass adds the in-CTA prefix itself.
-template <typename Col>
+template <typename Col, bool FUSED>
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                               uint64_t nseg, const Col* __restrict__ col,
-                                                              SegTot* seg_tot, SegTot* cta_tot, int tile_shift) {
+                                                              SegTot* seg_tot, SegTot* cta_tot, int tile_shift,
+                                                              FusedUpd fu, SegTot* cta_off, unsigned* ticket,
+                                                              LevelInfo* info, LevelParams lp) {
   __shared__ SegTot s_t[kScanThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
-  const SegTot t = seg < nseg ? count_seg(bm, nwords, seg, col, tile_shift) : SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
+  const SegTot t =
+      seg < nseg ? count_seg<Col, FUSED>(bm, nwords, seg, col, tile_shift, fu) : SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
   if (lane == 0) {
     if (seg < nseg) seg_tot[seg] = t;
     s_t[wid] = t;
   }
   __syncthreads();
+  __shared__ SegAcc s_scan[kScanThreads / 32 + 1];
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
     SegTot c{0u, 0u, 0u, 0u, 0ull, 0ull};
 #pragma unroll
     for (int w = 0; w < kScanThreads / 32; ++w)
       c = SegTot{c.cs + s_t[w].cs, c.na + s_t[w].na, c.nh + s_t[w].nh, 0u, c.ss + s_t[w].ss, c.ls + s_t[w].ls};
     cta_tot[blockIdx.x] = c;
+    __threadfence();  // the totals are visible before the ticket
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-}
-
-#ifndef BFS200_BLIND3
-#define BFS200_BLIND3 1
-#endif
-constexpr bool kBlind3 = BFS200_BLIND3;
-
-// Parent-claim mode thresholds (k_seg_scan; measured at s26): P2 when a row's
-// expected CSR scan is <= kP2Factor entries; mode 3 when the P1 candidate edges are >= rows / kM3Factor.
-constexpr ull kP2Factor = 8;
-constexpr ull kM3Factor = 4;
-
-// K3 scan of the per-CTA totals of the count pass, one CTA (the totals are few: one per 32 K
-// columns), fused with the level bookkeeping: seg_off[k] = exclusive scan of seg_tot[0..nseg)
-// (here: the CTA totals; seg_off[nseg] = the level's totals), then the per-level counters and the
-// parent-claim mode.  Pass k scans segments
-// [1024k, 1024k + 1024): warp inclusive scans by shuffles, the 32 warp totals scanned by warp 0
-// through shared memory, a running carry; the next pass's totals are loaded during this one.
-constexpr int kSegScanThreads = 1024;
-struct SegAcc {  // the scanned fields (pad is never summed)
-  unsigned cs, na, nh;
-  ull ss, ls;
-};
-__device__ __forceinline__ SegAcc seg_add(const SegAcc& a, const SegAcc& b) {
-  return SegAcc{a.cs + b.cs, a.na + b.na, a.nh + b.nh, a.ss + b.ss, a.ls + b.ls};
-}
-__device__ __forceinline__ SegAcc seg_sub(const SegAcc& a, const SegAcc& b) {
-  return SegAcc{a.cs - b.cs, a.na - b.na, a.nh - b.nh, a.ss - b.ss, a.ls - b.ls};
-}
-__device__ __forceinline__ SegAcc seg_shfl_up(const SegAcc& a, int d) {
-  return SegAcc{__shfl_up_sync(0xFFFFFFFFu, a.cs, d), __shfl_up_sync(0xFFFFFFFFu, a.na, d),
-                __shfl_up_sync(0xFFFFFFFFu, a.nh, d), __shfl_up_sync(0xFFFFFFFFu, a.ss, d),
-                __shfl_up_sync(0xFFFFFFFFu, a.ls, d)};
-}
-__device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t n) {
-  if (k >= n) return SegAcc{0u, 0u, 0u, 0ull, 0ull};
-  const SegTot t = p[k];
-  return SegAcc{t.cs, t.na, t.nh, t.ss, t.ls};
-}
-
-__global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
-                                                               SegTot* seg_off, LevelInfo* info, void* cumul, int narrow,
-                                                               ull nnz,
-                                                               ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
-  __shared__ SegAcc s_warp[kSegScanThreads / 32];
-  __shared__ SegAcc s_carry;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  SegAcc carry{0u, 0u, 0u, 0ull, 0ull};
-  SegAcc cur = seg_load(seg_tot, threadIdx.x, nseg);
-  for (uint64_t base = 0; base < nseg; base += kSegScanThreads) {
-    const SegAcc nxt = seg_load(seg_tot, base + kSegScanThreads + threadIdx.x, nseg);  // in flight
-    SegAcc inc = cur;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const SegAcc y = seg_shfl_up(inc, d);
-      if (lane >= d) inc = seg_add(inc, y);
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const SegAcc w = s_warp[lane];
-      SegAcc wi = w;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const SegAcc y = seg_shfl_up(wi, d);
-        if (lane >= d) wi = seg_add(wi, y);
-      }
-      s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
-      if (lane == 31) s_carry = wi;   // the pass total
-    }
-    __syncthreads();
-    const SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, cur)));
-    const uint64_t k = base + threadIdx.x;
-    if (k < nseg) seg_off[k] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
-    carry = seg_add(carry, s_carry);
-    __syncthreads();  // s_warp / s_carry are rewritten by the next pass
-    cur = nxt;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // every CTA's totals (ticketed before ours) are visible
+  const SegAcc tot = block_scan_totals<kScanThreads>(cta_tot, gridDim.x, cta_off, s_scan);
+  if (threadIdx.x == 0) {
+    level_bookkeeping(tot, gridDim.x, cta_off, info, lp);
+    *ticket = 0u;  // for the next level
   }
-  if (threadIdx.x != 0) return;
-  const SegAcc c = carry;
-  seg_off[nseg] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
-  // level totals; resets the per-level counters
-  info->n = c.cs;
-  info->sedges = c.ss;
-  info->nA = c.na;
-  info->edges = c.ss + c.ls;
-  info->ncols = c.cs;
-  info->newv = 0;
-  // Parent-claim mode of this level.  A discovered row's CSR scan stops at its first frontier
-  // neighbour, after ~nnz/edges entries on average (edges = entries leaving the frontier), so
-  // the scan (P2) is used when that is <= p2_factor (default 8); otherwise (small frontiers,
-  // e.g. the first levels) the expansion does atomicMin per candidate edge (P1).  P2 also when
-  // few rows remain to be discovered (the scans are then few, whatever their length):
-  // remaining = rows with entries - rows discovered so far (an estimate on this rank).
-  const ull edges = c.ss + c.ls, seen = info->disc_total;
-  const ull remaining = nz_rows > seen ? nz_rows - seen : 0ull;
-  info->mode = (edges * p2_factor >= nnz || remaining * 64ull <= edges) ? 2ull : 1ull;
-  // P1 with many candidate edges (mode 3): the expansion only claims (atomicMin); the parent
-  // pass derives the discovered words from pmin in one pass over the rows (cheaper than a
-  // RED.OR and a probe per edge once edges * m3_factor >= rows)
-  if (info->mode == 1 && m3_factor && edges * m3_factor >= nrows) info->mode = 3ull;
-  // mode 3 while at most 1/16 of the rows are visited (the first dense level): the visited
-  // probe of a non-hot row almost never finds the bit set, so the claim goes out without it
-  info->blind = (info->mode == 3 && kBlind3 && seen * 16ull <= nz_rows) ? 1ull : 0ull;
-  info->nlong = c.nh;  // hub columns, listed by k_scan_emit at scan positions
-  info->nlongcols = 0;
-  if (narrow) static_cast<uint32_t*>(cumul)[c.cs] = (uint32_t)c.ss;
-  else static_cast<ull*>(cumul)[c.cs] = c.ss;
 }
 
 // Emit pass: same word ownership.  Sparse chunks (< 96 set bits in 32 words): each lane totals
@@ -591,7 +668,8 @@ __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4*
   }
 }
 
-cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, cudaStream_t s) {
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, const LevelCtrl* ctrl,
+                        cudaStream_t s) {
   const uint64_t nwords = g.ncols() / 32;
   const uint64_t nseg = (nwords + kScanSegWords - 1) / kScanSegWords;
   const unsigned grid = (unsigned)((nseg + kScanThreads / 32 - 1) / (kScanThreads / 32));
@@ -600,11 +678,19 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   SegTot* ct = static_cast<SegTot*>(rk.seg_off);  // [grid] CTA totals, then [grid + 1] their scan
   SegTot* co = ct + grid;
   // narrow: the 32-bit copy of the column offsets (half the bytes of the col[] reads)
-  if (narrow) k_scan_count<uint32_t><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts);
-  else k_scan_count<ull><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts);
-  // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
-  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows,
-                                          kM3Factor, (ull)g.nrows());
+  const FusedUpd fu{rk.vis, rk.vold, rk.all_front, rk.level, ctrl};
+  const LevelParams lp{rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows, kM3Factor, (ull)g.nrows()};
+  if (ctrl) {  // fused update (1x1): narrow or not
+    if (narrow)
+      k_scan_count<uint32_t, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+    else
+      k_scan_count<ull, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+  } else if (narrow) {
+    k_scan_count<uint32_t, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+  } else {
+    k_scan_count<ull, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+  }
+
   if (narrow)
     k_scan_emit<true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, co, rk.flist, rk.rowoff,
                                                     rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
@@ -1318,7 +1404,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
                                                                const uint32_t* __restrict__ inv_col,
                                                                LevelInfo* info, uint32_t hot_words, int R,
                                                                uint64_t Wc, int blog,
-                                                               uint32_t* const* __restrict__ fold_dst) {
+                                                               uint32_t* const* __restrict__ fold_dst, int fused) {
   extern __shared__ __align__(16) unsigned char psmem[];
   uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
@@ -1536,14 +1622,17 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) ndisc += __shfl_xor_sync(0xFFFFFFFFu, ndisc, o);
-  if (lane == 0 && ndisc) atomicAdd(&info->disc_total, (ull)ndisc);
+  if (lane == 0 && ndisc) {
+    atomicAdd(&info->disc_total, (ull)ndisc);
+    if (fused) atomicAdd(&info->newv, (ull)ndisc);  // no K2 (1x1): the level's new vertices, counted here
+  }
   if (fold_dst) {  // the CTA's peer stores, then one system-scope fence (cumulative) before the flag
     __syncthreads();
     if (threadIdx.x == 0) __threadfence_system();
   }
 }
 
-cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
+cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, cudaStream_t s) {
   const uint64_t nwords = g.nrows() / 32;
   const uint64_t nchunks = (nwords + 31) / 32;
   uint64_t grid = (nchunks + kParentThreads / 32 - 1) / (kParentThreads / 32);
@@ -1561,7 +1650,7 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s) {
   k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vis, rk.vold, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
                                                         rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
                                                         (uint32_t)hw, g.R, g.words_block(), blog,
-                                                        g.C > 1 ? rk.fold_dst : nullptr);
+                                                        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -8,13 +8,18 @@ namespace bfs200 {
 cudaError_t kernels_init_device();
 
 // Alg.2 init lines P:334-343: reset per-search state of one rank and seed the root on its owner.
-cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, cudaStream_t s);
+// fused: the frontier update of a 1x1 graph runs in the next level's count pass (no K2; see
+// FusedUpd in kernels.cu): the root is seeded into vis only
+cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, bool fused, cudaStream_t s);
 
 // K3: frontier bitmap (ncols bits) -> ascending list of columns with degree > 0, their row
 // offsets and the exclusive scan of their degrees.
 // narrow: every CSC position of the rank fits in 32 bits and K1 runs its POS32 variant (the row
 // offsets and the degree scan are then written as 32-bit values)
-cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, cudaStream_t s);
+// ctrl != null: fused frontier update of a 1x1 graph (the count pass builds the frontier from
+// vis & ~vold, advances vold, writes the previous level's levels)
+cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narrow, const LevelCtrl* ctrl,
+                        cudaStream_t s);
 
 // K1: top-down frontier expansion (Alg.3, grouped edges P:565-586).
 cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_t hot_h, bool force_pos64,
@@ -22,7 +27,7 @@ cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_
 uint32_t expand_tile_edges(int edges_per_thread);
 
 // K4: parent claim for the rows discovered in this level (+ pack of the fold message, C > 1).
-cudaError_t launch_parent(const Geom& g, Rank& rk, cudaStream_t s);
+cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, cudaStream_t s);
 
 // K2: frontier update + pack; lvl is the level being assigned.
 cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s);
