@@ -108,7 +108,6 @@ struct Rank {
   uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
   void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
   void* seg_off = nullptr;               // [nseg+1] K3 scratch: per-CTA totals of the count pass and their scan
-  unsigned* scan_ticket = nullptr;       // [1] K3: CTAs of the count pass done (the last one scans)
   uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution

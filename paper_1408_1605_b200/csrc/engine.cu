@@ -207,8 +207,6 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
   AL(rk.seg_tot, (nseg + 1) * 32);
   AL(rk.seg_off, (nseg + 8) * 32);  // CTA totals (nseg/8 + 1) and their scan (nseg/8 + 2)
-  AL(rk.scan_ticket, 16);
-  CKR(cudaMemsetAsync(rk.scan_ticket, 0, 16, G.stream));
   CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
   AL(rk.parent_tmp, g.block * 8);
   AL(rk.level_tmp, g.block * 4);
@@ -1003,13 +1001,13 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     }
     stats->reached = 0;
     // own kernels: seed (owner only), level_begin, per level level_end and per local rank
-    // scan(3) + expand + parent + update (no update on a fused 1x1 graph), then finalize; with C > 1 the resolution adds
+    // scan(4) + expand + parent + update (no update on a fused 1x1 graph), then finalize; with C > 1 the resolution adds
     // req_build, 2 seg_totals and resp_pack.
     const uint64_t nl = G.ranks.size();
     const bool peer = peer_active(G);
     const int owner_j = (int)(owner / (uint64_t)g.R);
     stats->kernel_launches =
-        (owner_local ? 1 : 0) + 1 + nlev + nl * ((fused_of(G) ? 5ull : 6ull) * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
+        (owner_local ? 1 : 0) + 1 + nlev + nl * ((fused_of(G) ? 6ull : 7ull) * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
         G.xlaunches +
         (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
   }

@@ -151,12 +151,13 @@ constexpr bool kBlind3 = BFS200_BLIND3;
 constexpr ull kP2Factor = 8;
 constexpr ull kM3Factor = 4;
 
-// K3 scan of the per-CTA totals of the count pass, fused into that pass: the last CTA to finish
-// (an atomic ticket after each CTA's totals are written and fenced) scans the CTA totals --
-// each thread sums up to kScanItems consecutive totals, one block scan of the thread sums, the
-// exclusive prefixes written back (seg_off[n] = the level's totals) -- and does the level
-// bookkeeping (counts, parent-claim mode).  No separate launch, no library scan.
-constexpr int kScanItems = 8;
+// K3 scan of the per-CTA totals of the count pass, one CTA (the totals are few: one per 32 K
+// columns), fused with the level bookkeeping: seg_off[k] = exclusive scan of seg_tot[0..nseg)
+// (here: the CTA totals; seg_off[nseg] = the level's totals), then the per-level counters and the
+// parent-claim mode.  Pass k scans segments
+// [1024k, 1024k + 1024): warp inclusive scans by shuffles, the 32 warp totals scanned by warp 0
+// through shared memory, a running carry; the next pass's totals are loaded during this one.
+constexpr int kSegScanThreads = 1024;
 struct SegAcc {  // the scanned fields (pad is never summed)
   unsigned cs, na, nh;
   ull ss, ls;
@@ -172,29 +173,24 @@ __device__ __forceinline__ SegAcc seg_shfl_up(const SegAcc& a, int d) {
                 __shfl_up_sync(0xFFFFFFFFu, a.nh, d), __shfl_up_sync(0xFFFFFFFFu, a.ss, d),
                 __shfl_up_sync(0xFFFFFFFFu, a.ls, d)};
 }
-// (L2 loads: the totals were written by other CTAs of the same kernel)
 __device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t n) {
   if (k >= n) return SegAcc{0u, 0u, 0u, 0ull, 0ull};
-  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p + k);
-  const ulonglong2 a = __ldcg(q), b = __ldcg(q + 1);  // {cs | na << 32, nh | pad << 32}, {ss, ls}
-  return SegAcc{(unsigned)a.x, (unsigned)(a.x >> 32), (unsigned)a.y, b.x, b.y};
+  const SegTot t = p[k];
+  return SegAcc{t.cs, t.na, t.nh, t.ss, t.ls};
 }
 
-
-// exclusive scan of tot[0..n) into off[0..n], by the NT threads of one CTA; returns the total
-template <int NT>
-__device__ __forceinline__ SegAcc block_scan_totals(const SegTot* tot, uint64_t n, SegTot* off, SegAcc* s_warp) {
+__global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
+                                                               SegTot* seg_off, LevelInfo* info, void* cumul, int narrow,
+                                                               ull nnz,
+                                                               ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
+  __shared__ SegAcc s_warp[kSegScanThreads / 32];
+  __shared__ SegAcc s_carry;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   SegAcc carry{0u, 0u, 0u, 0ull, 0ull};
-  for (uint64_t base = 0; base < n; base += (uint64_t)NT * kScanItems) {
-    const uint64_t k0 = base + (uint64_t)threadIdx.x * kScanItems;
-    SegAcc v[kScanItems];
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q) v[q] = seg_load(tot, k0 + q, n);  // all in flight
-    SegAcc mine{0u, 0u, 0u, 0ull, 0ull};
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q) mine = seg_add(mine, v[q]);
-    SegAcc inc = mine;
+  SegAcc cur = seg_load(seg_tot, threadIdx.x, nseg);
+  for (uint64_t base = 0; base < nseg; base += kSegScanThreads) {
+    const SegAcc nxt = seg_load(seg_tot, base + kSegScanThreads + threadIdx.x, nseg);  // in flight
+    SegAcc inc = cur;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const SegAcc y = seg_shfl_up(inc, d);
@@ -203,42 +199,27 @@ __device__ __forceinline__ SegAcc block_scan_totals(const SegTot* tot, uint64_t 
     if (lane == 31) s_warp[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-      const SegAcc w = lane < NT / 32 ? s_warp[lane] : SegAcc{0u, 0u, 0u, 0ull, 0ull};
+      const SegAcc w = s_warp[lane];
       SegAcc wi = w;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const SegAcc y = seg_shfl_up(wi, d);
         if (lane >= d) wi = seg_add(wi, y);
       }
-      if (lane < NT / 32) s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
-      if (lane == 31) s_warp[NT / 32] = wi;               // the pass total
+      s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
+      if (lane == 31) s_carry = wi;   // the pass total
     }
     __syncthreads();
-    SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, mine)));
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q) {
-      if (k0 + q < n) off[k0 + q] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
-      ex = seg_add(ex, v[q]);
-    }
-    carry = seg_add(carry, s_warp[NT / 32]);
-    __syncthreads();  // s_warp is rewritten by the next pass
+    const SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, cur)));
+    const uint64_t k = base + threadIdx.x;
+    if (k < nseg) seg_off[k] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
+    carry = seg_add(carry, s_carry);
+    __syncthreads();  // s_warp / s_carry are rewritten by the next pass
+    cur = nxt;
   }
-  return carry;
-}
-
-// the level's totals and bookkeeping (one thread)
-struct LevelParams {
-  void* cumul;
-  int narrow;
-  ull nnz, p2_factor, nz_rows, m3_factor, nrows;
-};
-__device__ __forceinline__ void level_bookkeeping(const SegAcc& c, uint64_t n, SegTot* seg_off, LevelInfo* info,
-                                                  const LevelParams& lp) {
-  const ull nnz = lp.nnz, p2_factor = lp.p2_factor, nz_rows = lp.nz_rows, m3_factor = lp.m3_factor,
-            nrows = lp.nrows;
-  void* cumul = lp.cumul;
-  const int narrow = lp.narrow;
-  seg_off[n] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
+  if (threadIdx.x != 0) return;
+  const SegAcc c = carry;
+  seg_off[nseg] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
   // level totals; resets the per-level counters
   info->n = c.cs;
   info->sedges = c.ss;
@@ -398,14 +379,13 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
 }
 
 // Per-segment totals (seg_tot[seg]) and per-CTA totals of the kScanThreads/32 segments of a CTA
-// (cta_tot[b]): the last CTA then scans only the few CTA totals (block_scan_totals), and the
+// (cta_tot[b]): the single-CTA scan (k_seg_scan) then only scans the few CTA totals, and the
 // emit pass adds the in-CTA prefix itself.
 template <typename Col, bool FUSED>
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                               uint64_t nseg, const Col* __restrict__ col,
                                                               SegTot* seg_tot, SegTot* cta_tot, int tile_shift,
-                                                              FusedUpd fu, SegTot* cta_off, unsigned* ticket,
-                                                              LevelInfo* info, LevelParams lp) {
+                                                              FusedUpd fu) {
   __shared__ SegTot s_t[kScanThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
@@ -416,24 +396,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __r
     s_t[wid] = t;
   }
   __syncthreads();
-  __shared__ SegAcc s_scan[kScanThreads / 32 + 1];
-  __shared__ bool s_last;
   if (threadIdx.x == 0) {
     SegTot c{0u, 0u, 0u, 0u, 0ull, 0ull};
 #pragma unroll
     for (int w = 0; w < kScanThreads / 32; ++w)
       c = SegTot{c.cs + s_t[w].cs, c.na + s_t[w].na, c.nh + s_t[w].nh, 0u, c.ss + s_t[w].ss, c.ls + s_t[w].ls};
     cta_tot[blockIdx.x] = c;
-    __threadfence();  // the totals are visible before the ticket
-    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();  // every CTA's totals (ticketed before ours) are visible
-  const SegAcc tot = block_scan_totals<kScanThreads>(cta_tot, gridDim.x, cta_off, s_scan);
-  if (threadIdx.x == 0) {
-    level_bookkeeping(tot, gridDim.x, cta_off, info, lp);
-    *ticket = 0u;  // for the next level
   }
 }
 
@@ -679,18 +647,20 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   SegTot* co = ct + grid;
   // narrow: the 32-bit copy of the column offsets (half the bytes of the col[] reads)
   const FusedUpd fu{rk.vis, rk.vold, rk.all_front, rk.level, ctrl};
-  const LevelParams lp{rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor, (ull)rk.nz_rows, kM3Factor, (ull)g.nrows()};
   if (ctrl) {  // fused update (1x1): narrow or not
     if (narrow)
-      k_scan_count<uint32_t, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+      k_scan_count<uint32_t, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu);
     else
-      k_scan_count<ull, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+      k_scan_count<ull, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu);
   } else if (narrow) {
-    k_scan_count<uint32_t, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+    k_scan_count<uint32_t, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu);
   } else {
-    k_scan_count<ull, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu, co, rk.scan_ticket, rk.info, lp);
+    k_scan_count<ull, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu);
   }
 
+  // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
+  k_seg_scan<<<1, kSegScanThreads, 0, s>>>(ct, grid, co, rk.info, rk.cumul, narrow ? 1 : 0, (ull)rk.nnz, kP2Factor,
+                                          (ull)rk.nz_rows, kM3Factor, (ull)g.nrows());
   if (narrow)
     k_scan_emit<true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, co, rk.flist, rk.rowoff,
                                                     rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
