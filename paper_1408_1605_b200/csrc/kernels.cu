@@ -1869,22 +1869,49 @@ cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_
 }
 
 // ------------------------------------------------------------------ parent resolution (C > 1)
-// request bitmaps: req[c] has bit t for owned reached t whose winner column is c != j
+// request bitmaps: req[c] has bit t for owned reached t whose winner column is c != j.  A warp
+// takes 32 consecutive words; for word k lane l reads the winner of vertex 32k + l (coalesced) and
+// one ballot per column builds the word (C <= 8; wider grids take the per-bit loop).
 __global__ void k_req_build(const uint32_t* vis_own, const uint8_t* winner, uint32_t* req, uint64_t W, int C, int j) {
+  const int lane = threadIdx.x & 31;
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= W) return;
-  uint32_t b = vis_own[w];  // visited word
-  while (b) {
-    const int bit = __ffs(b) - 1;
-    b &= b - 1;
-    const int c = winner[w * 32 + bit];
-    if (c != j) req[(uint64_t)c * W + w] |= 1u << bit;
+  const uint32_t vb = w < W ? vis_own[w] : 0u;  // visited word
+  if (C > 8) {
+    if (w >= W) return;
+    for (int c = 0; c < C; ++c) req[(uint64_t)c * W + w] = 0u;
+    uint32_t b = vb;
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      const int c = winner[w * 32 + bit];
+      if (c != j) req[(uint64_t)c * W + w] |= 1u << bit;
+    }
+    return;
   }
+  const uint64_t w0 = w - lane;
+  uint32_t r[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // lane l: request word of w0 + l per column
+  unsigned nz = __ballot_sync(0xFFFFFFFFu, vb != 0u);
+  while (nz) {
+    const int k = __ffs(nz) - 1;
+    nz &= nz - 1;
+    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, vb, k);
+    const bool reached = (bk >> lane) & 1u;
+    const int c = reached ? (int)winner[(w0 + k) * 32 + lane] : j;
+#pragma unroll
+    for (int c2 = 0; c2 < 8; ++c2) {
+      if (c2 >= C) break;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, c == c2 && c2 != j);
+      if (lane == k) r[c2] = m;
+    }
+  }
+  if (w < W)
+#pragma unroll
+    for (int c2 = 0; c2 < 8; ++c2)
+      if (c2 < C) req[(uint64_t)c2 * W + w] = r[c2];
 }
 
 cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s) {
   const uint64_t W = g.words_block();
-  cudaMemsetAsync(rk.req, 0, W * g.C * 4, s);
   k_req_build<<<(unsigned)((W + 255) / 256), 256, 0, s>>>(rk.vis + (uint64_t)rk.j * W, rk.winner, rk.req, W,
                                                            g.C, rk.j);
   return cudaGetLastError();
@@ -1910,20 +1937,29 @@ cudaError_t launch_popc_scan(const uint32_t* bits, uint32_t* off, uint64_t nword
 }
 
 // responder: for every requesting column c != j, pack pred of the requested rows of segment c
-// in ascending order into resp[c*block ...]
+// in ascending order into resp[c*block ...].  A warp takes 32 consecutive request words of one
+// segment; for word k lane l moves row 32k + l (coalesced pred read, contiguous writes at the
+// word's scan offset + the requested rows below it).
 __global__ void k_resp_pack(const uint32_t* reqin, const uint32_t* off, const uint32_t* pred, uint32_t* resp,
                             uint64_t W, uint64_t block, int C, int j) {
+  const int lane = threadIdx.x & 31;
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= W * (uint64_t)C) return;
-  const int c = (int)(gid / W);
-  if (c == j) return;
-  const uint64_t w = gid - (uint64_t)c * W;
-  uint32_t b = reqin[gid];
-  uint64_t pos = off[gid] - off[(uint64_t)c * W];
-  while (b) {
-    const int bit = __ffs(b) - 1;
-    b &= b - 1;
-    resp[(uint64_t)c * block + pos++] = pred[(uint64_t)c * block + w * 32 + bit];
+  const bool in = gid < W * (uint64_t)C;
+  const int c = in ? (int)(gid / W) : j;
+  const uint32_t b = (in && c != j) ? reqin[gid] : 0u;
+  const uint64_t pos = b ? off[gid] - off[(uint64_t)c * W] : 0ull;
+  const uint64_t w = in ? gid - (uint64_t)c * W : 0ull;
+  const unsigned lt = lanemask_lt();
+  unsigned nz = __ballot_sync(0xFFFFFFFFu, b != 0u);
+  while (nz) {
+    const int k = __ffs(nz) - 1;
+    nz &= nz - 1;
+    const uint32_t bk = __shfl_sync(0xFFFFFFFFu, b, k);
+    const uint64_t pk = __shfl_sync(0xFFFFFFFFu, pos, k);
+    const uint64_t wk = __shfl_sync(0xFFFFFFFFu, w, k);
+    const int ck = __shfl_sync(0xFFFFFFFFu, c, k);
+    if ((bk >> lane) & 1u)
+      resp[(uint64_t)ck * block + pk + __popc(bk & lt)] = pred[(uint64_t)ck * block + wk * 32 + lane];
   }
 }
 
