@@ -179,18 +179,21 @@ __device__ __forceinline__ SegAcc seg_load(const SegTot* p, uint64_t k, uint64_t
   return SegAcc{t.cs, t.na, t.nh, t.ss, t.ls};
 }
 
-__global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
-                                                               SegTot* seg_off, LevelInfo* info, void* cumul, int narrow,
-                                                               ull nnz,
-                                                               ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
-  __shared__ SegAcc s_warp[kSegScanThreads / 32];
-  __shared__ SegAcc s_carry;
+constexpr int kSegItems = 2;  // consecutive totals per thread and pass (2048 per pass)
+// exclusive scan of tot[0..n) into off[0..n], by the NT threads of one CTA; returns the total
+template <int NT>
+__device__ __forceinline__ SegAcc block_scan_totals(const SegTot* tot, uint64_t n, SegTot* off, SegAcc* s_warp) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   SegAcc carry{0u, 0u, 0u, 0ull, 0ull};
-  SegAcc cur = seg_load(seg_tot, threadIdx.x, nseg);
-  for (uint64_t base = 0; base < nseg; base += kSegScanThreads) {
-    const SegAcc nxt = seg_load(seg_tot, base + kSegScanThreads + threadIdx.x, nseg);  // in flight
-    SegAcc inc = cur;
+  for (uint64_t base = 0; base < n; base += (uint64_t)NT * kSegItems) {
+    const uint64_t k0 = base + (uint64_t)threadIdx.x * kSegItems;
+    SegAcc v[kSegItems];
+#pragma unroll
+    for (int q = 0; q < kSegItems; ++q) v[q] = seg_load(tot, k0 + q, n);  // all in flight
+    SegAcc mine{0u, 0u, 0u, 0ull, 0ull};
+#pragma unroll
+    for (int q = 0; q < kSegItems; ++q) mine = seg_add(mine, v[q]);
+    SegAcc inc = mine;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const SegAcc y = seg_shfl_up(inc, d);
@@ -199,24 +202,35 @@ __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __re
     if (lane == 31) s_warp[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-      const SegAcc w = s_warp[lane];
+      const SegAcc w = lane < NT / 32 ? s_warp[lane] : SegAcc{0u, 0u, 0u, 0ull, 0ull};
       SegAcc wi = w;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const SegAcc y = seg_shfl_up(wi, d);
         if (lane >= d) wi = seg_add(wi, y);
       }
-      s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
-      if (lane == 31) s_carry = wi;   // the pass total
+      if (lane < NT / 32) s_warp[lane] = seg_sub(wi, w);  // exclusive over the warps
+      if (lane == 31) s_warp[NT / 32] = wi;               // the pass total
     }
     __syncthreads();
-    const SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, cur)));
-    const uint64_t k = base + threadIdx.x;
-    if (k < nseg) seg_off[k] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
-    carry = seg_add(carry, s_carry);
-    __syncthreads();  // s_warp / s_carry are rewritten by the next pass
-    cur = nxt;
+    SegAcc ex = seg_add(carry, seg_add(s_warp[wid], seg_sub(inc, mine)));
+#pragma unroll
+    for (int q = 0; q < kSegItems; ++q) {
+      if (k0 + q < n) off[k0 + q] = SegTot{ex.cs, ex.na, ex.nh, 0u, ex.ss, ex.ls};
+      ex = seg_add(ex, v[q]);
+    }
+    carry = seg_add(carry, s_warp[NT / 32]);
+    __syncthreads();  // s_warp is rewritten by the next pass
   }
+  return carry;
+}
+
+__global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __restrict__ seg_tot, uint64_t nseg,
+                                                               SegTot* seg_off, LevelInfo* info, void* cumul, int narrow,
+                                                               ull nnz,
+                                                               ull p2_factor, ull nz_rows, ull m3_factor, ull nrows) {
+  __shared__ SegAcc s_warp[kSegScanThreads / 32 + 1];
+  const SegAcc carry = block_scan_totals<kSegScanThreads>(seg_tot, nseg, seg_off, s_warp);
   if (threadIdx.x != 0) return;
   const SegAcc c = carry;
   seg_off[nseg] = SegTot{c.cs, c.na, c.nh, 0u, c.ss, c.ls};
@@ -449,6 +463,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   // compact 8-byte long-tile records (position, length) in P2 levels of the pipelined loop (the
   // column is only needed by the P1 claims): half the record traffic of K3 and K1
   const bool compact = NARROW && BFS200_K1PIPE > 0 && info->mode == 2 && tile_shift <= 8;
+  const bool need_flist = info->mode != 2;  // the column ids of short columns: P1 claims only
   auto emit_long = [&](uint64_t u, ull c0, ull d, uint64_t pa, unsigned nt, uint64_t hub) {
     if (nt <= 8) {
       for (unsigned q = 0; q < nt; ++q) {
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
             const uint64_t pos = k + __popc(smask & lt);
             const ull eb = e + inc - ds;
             BCHECK(pos < info->cap_ncols && u < info->cap_ncols && c0 + ds <= info->cap_nnz);
-            flist[pos] = (uint32_t)u;
+            if (need_flist) flist[pos] = (uint32_t)u;
             rowoff[pos] = (Off)c0;
             cumul[pos] = (Off)eb;
             for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) {
@@ -595,7 +610,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         ++nlongcols;
       } else if (d) {
         BCHECK(kk < info->cap_ncols && u < info->cap_ncols && c0 + d <= info->cap_nnz);
-        flist[kk] = (uint32_t)u;
+        if (need_flist) flist[kk] = (uint32_t)u;
         rowoff[kk] = (Off)c0;
         cumul[kk] = (Off)ee;
         for (ull t = (ee + tm) >> tile_shift; (t << tile_shift) < ee + d; ++t) {
