@@ -29,6 +29,10 @@ namespace bfs200 {
 
 typedef unsigned long long ull;
 
+// the pipelined short-tile loop of K1 in P2 levels (short_tiles_p2; 0 = the staged loop)
+#ifndef BFS200_SHORTPIPE
+#define BFS200_SHORTPIPE 1
+#endif
 // row slots of the pipelined long-tile loop of K1 (long_tiles_p2; 0 = the double-buffered loop)
 #ifndef BFS200_K1PIPE
 #define BFS200_K1PIPE 3
@@ -987,6 +991,250 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
   }
 }
 
+// Edge -> column mapping of one 32-edge window of a short tile, in registers (the paper's
+// binary search of the scan, P:455-470 / Alg.3 line 2).  Lane l holds CS of the tile's columns,
+// l + 32c: beg = the column's first edge relative to the tile (0 for a column begun in an
+// earlier tile; TILE for lanes past the tile's last column) and base = its row offset minus its
+// scan value (row position of short edge g of the column = base + g, modular when Pos is 32-bit).
+// Columns have distinct starts (a short column has degree >= 1), so edge lo + lane belongs to
+// column k = #(columns starting before the window) + #(columns starting in the window at or
+// before the edge) - 1: one ballot and one OR-reduction of start bits per column set, a popcount,
+// then a shuffle of base from the lane holding column k.
+template <int CS, typename Pos>
+__device__ __forceinline__ Pos short_map(const uint32_t (&beg)[CS], const Pos (&base)[CS], uint32_t lo, int lane) {
+  uint32_t sb = 0, before = 0;
+#pragma unroll
+  for (int c = 0; c < CS; ++c) {
+    const uint32_t r = beg[c] - lo;  // in the window when r < 32 (unsigned)
+    sb |= __reduce_or_sync(0xFFFFFFFFu, r < 32u ? 1u << r : 0u);
+    before += __popc(__ballot_sync(0xFFFFFFFFu, beg[c] < lo));
+  }
+  const uint32_t k = before + __popc(sb & (0xFFFFFFFFu >> (31 - lane))) - 1u;
+  Pos b = __shfl_sync(0xFFFFFFFFu, base[0], (int)(k & 31u));
+#pragma unroll
+  for (int c = 1; c < CS; ++c) {
+    const Pos bc = __shfl_sync(0xFFFFFFFFu, base[c], (int)(k & 31u));
+    b = (k >> 5) == (uint32_t)c ? bc : b;
+  }
+  return b;
+}
+
+// Register-lean probe / RED for the short-tile loop (its pipeline state leaves no room for
+// probe4's mask and address): the probe leaves x = 0xFFFFFFFF when no RED is due (hot and
+// visited, or no row), else the loaded visited word; the RED recomputes the bit and the word
+// address from v.  Two live registers per row instead of five.
+template <bool SEG1>
+__device__ __forceinline__ uint32_t probe_lean(uint32_t v, uint32_t hw, uint32_t sa, const uint32_t* vis, int bl,
+                                               uint32_t bmask) {
+  uint32_t x;
+  if (SEG1) {
+    asm("{\n"
+        " .reg .pred pok, pn;\n"
+        " .reg .b32 wi, hi, hv, m;\n"
+        " .reg .b64 a;\n"
+        " setp.ne.u32 pok, %1, 0xFFFFFFFF;\n"
+        " shr.b32 wi, %1, 5;\n"
+        " min.u32 hi, wi, %2;\n"
+        " shl.b32 hi, hi, 2;\n"
+        " add.u32 hi, hi, %3;\n"
+        " ld.shared.u32 hv, [hi];\n"
+        " shf.l.wrap.b32 m, 0, 1, %1;\n"
+        " and.b32 hv, hv, m;\n"
+        " setp.eq.and.b32 pn, hv, 0, pok;\n"
+        " mov.b32 %0, 0xFFFFFFFF;\n"
+        " mad.wide.u32 a, wi, 4, %4;\n"
+        " @pn ld.global.cg.u32 %0, [a];\n"
+        "}"
+        : "=r"(x)
+        : "r"(v), "r"(hw), "r"(sa), "l"(vis));
+  } else {
+    asm("{\n"
+        " .reg .pred pok, pn;\n"
+        " .reg .b32 wi, hi, hv, m, sg, off;\n"
+        " .reg .b64 a;\n"
+        " setp.ne.u32 pok, %1, 0xFFFFFFFF;\n"
+        " shr.b32 wi, %1, 5;\n"
+        " shr.b32 sg, %1, %5;\n"
+        " and.b32 off, %1, %6;\n"
+        " shr.b32 off, off, 5;\n"
+        " min.u32 off, off, %2;\n"
+        " add.u32 hv, %2, 1;\n"
+        " mad.lo.u32 hi, sg, hv, off;\n"
+        " selp.u32 hi, hi, %2, pok;\n"
+        " shl.b32 hi, hi, 2;\n"
+        " add.u32 hi, hi, %3;\n"
+        " ld.shared.u32 hv, [hi];\n"
+        " shf.l.wrap.b32 m, 0, 1, %1;\n"
+        " and.b32 hv, hv, m;\n"
+        " setp.eq.and.b32 pn, hv, 0, pok;\n"
+        " mov.b32 %0, 0xFFFFFFFF;\n"
+        " mad.wide.u32 a, wi, 4, %4;\n"
+        " @pn ld.global.cg.u32 %0, [a];\n"
+        "}"
+        : "=r"(x)
+        : "r"(v), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
+  }
+  return x;
+}
+__device__ __forceinline__ void red_lean(uint32_t x, uint32_t v, uint32_t* vis) {
+  asm volatile("{\n"
+               " .reg .pred pr;\n"
+               " .reg .b32 m, t, wi;\n"
+               " .reg .b64 a;\n"
+               " shf.l.wrap.b32 m, 0, 1, %1;\n"
+               " and.b32 t, %0, m;\n"
+               " setp.eq.b32 pr, t, 0;\n"
+               " shr.b32 wi, %1, 5;\n"
+               " mad.wide.u32 a, wi, 4, %2;\n"
+               " @pr red.relaxed.gpu.global.or.b32 [a], m;\n"
+               "}" ::"r"(x), "r"(v), "l"(vis));
+}
+
+// One short tile of more than 32 columns (runs of degree-1..3 columns) of a P2 level: its table
+// entries, columns (E sets per lane, short_map) and rows loaded in one go, then the visited tests
+// and RED.ORs.  Not inlined: its column registers would otherwise be allocated on top of the whole
+// pipeline state of short_tiles_p2 (which then spilled the row slots).
+template <int E, bool SEG1, bool POS32>
+__device__ __noinline__ void short_wide_tile(const uint32_t* __restrict__ row, const uint32_t* __restrict__ tile_k,
+                                             const void* __restrict__ rowoff_v, const void* __restrict__ cumul_v,
+                                             uint32_t n, ull total, uint32_t ntiles, uint32_t t, uint32_t* vis,
+                                             uint32_t hw, uint32_t sa, int bl, uint32_t bmask, int lane,
+                                             const LevelInfo* info) {
+  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  constexpr int TILE = 32 * E;
+  const Pos* __restrict__ rowoff = static_cast<const Pos*>(rowoff_v);
+  const Pos* __restrict__ cumul = static_cast<const Pos*>(cumul_v);
+  const uint32_t klo = tile_k[t];
+  const uint32_t cnt = (t + 1 < ntiles ? tile_k[t + 1] : n - 1) - klo + 1u;
+  BCHECK(cnt > 32u && cnt <= (uint32_t)TILE + 1 && klo + cnt <= n);
+  const Pos tb = (Pos)t * TILE;
+  uint32_t beg[E];
+  Pos base[E];
+#pragma unroll
+  for (int c = 0; c < E; ++c) {
+    const uint32_t idx = 32u * c + lane;
+    Pos rc = ~(Pos)0, ro = 0;
+    if (idx < cnt) {
+      rc = cumul[klo + idx];
+      ro = rowoff[klo + idx];
+    }
+    beg[c] = rc > tb ? (uint32_t)min(rc - tb, (Pos)TILE) : 0u;
+    base[c] = (Pos)(ro - rc);
+  }
+  uint32_t vv[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const Pos g = tb + 32u * e + lane;
+    const Pos b = short_map<E, Pos>(beg, base, 32u * e, lane);
+    vv[e] = 0xFFFFFFFFu;
+    ld_stream_u32_if(g < (Pos)total, row + (Pos)(b + g), vv[e]);  // Alg.3 line 4
+  }
+  uint32_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
+    BCHECK(vv[e] == 0xFFFFFFFFu || vv[e] < info->cap_nrows);
+    x[e] = probe_lean<SEG1>(vv[e], hw, sa, vis, bl, bmask);
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) red_lean(x[e], vv[e], vis);  // Alg.3 line 7
+}
+
+// Short-column tiles of a P2 level, software-pipelined like long_tiles_p2.  Warp tile q (tile id
+// t0 + q*stride) covers short edges [32E*tile, 32E*tile + 32E) of the level's scan; its columns
+// are klo .. khi of the short list (tile_k), cnt <= 32E of them.  Tiles of cnt <= 32 columns (the
+// bulk of the edges: short columns average more than 4 edges) keep one column per lane and run
+// four stages one phase apart -- phase q: the tile-table entries of tile q+3, the column loads
+// (scan value, row offset) of tile q+2, the mapping (short_map) and row loads of tile q+1, the
+// visited tests and RED.ORs of tile q (Alg.3 lines 4-7) -- so no load is waited on in the phase
+// that issues it.  Slots are compile-time indices of a loop unrolled four times.  A tile of more
+// than 32 columns (runs of degree-1..3 columns) is loaded, mapped (all E column sets per lane)
+// and tested in its own phase, outside the pipeline.
+template <int E, bool SEG1, bool POS32>
+__device__ __noinline__ void short_tiles_p2(const uint32_t* __restrict__ row, const uint32_t* __restrict__ tile_k,
+                                            const void* __restrict__ rowoff_v, const void* __restrict__ cumul_v,
+                                            uint32_t n, ull total, uint32_t ntiles, uint32_t t0, uint32_t stride,
+                                            uint32_t* vis, uint32_t hw, uint32_t sa, int bl, uint32_t bmask, int lane,
+                                            const LevelInfo* info) {
+  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;  // also edge counts (total < 2^32 when POS32)
+  constexpr int TILE = 32 * E;
+  constexpr int NS = 4;
+  constexpr uint32_t kWide = 0xFFFFFFFEu;  // v[s][0] of a tile of > 32 columns (never a row id: rows < 2^32 - 1)
+  const Pos* __restrict__ rowoff = static_cast<const Pos*>(rowoff_v);
+  const Pos* __restrict__ cumul = static_cast<const Pos*>(cumul_v);
+  const Pos tot = (Pos)total;
+  uint32_t mklo[NS], mcnt[NS];  // table entries: first column, column count (0 past the warp's last tile)
+  Pos crc[NS], cro[NS];         // the lane's column: scan value, row offset (raw loads)
+  uint32_t v[NS][E];            // row ids; 0xFFFFFFFF past the tile's end; kWide: a tile of > 32 columns
+  auto meta_load = [&](int s, uint32_t t) {
+    mcnt[s] = 0u;
+    mklo[s] = 0u;
+    if (t < ntiles) {
+      const uint32_t klo = tile_k[t];
+      const uint32_t khi = t + 1 < ntiles ? tile_k[t + 1] : n - 1;
+      BCHECK(klo <= khi && khi < n && khi - klo < (uint32_t)TILE + 1);
+      mklo[s] = klo;
+      mcnt[s] = khi - klo + 1u;
+    }
+  };
+  auto cols_load = [&](int s) {
+    crc[s] = ~(Pos)0;  // no column: beg clamps to TILE
+    cro[s] = 0;
+    if (mcnt[s] <= 32u && (uint32_t)lane < mcnt[s]) {
+      crc[s] = cumul[mklo[s] + lane];
+      cro[s] = rowoff[mklo[s] + lane];
+    }
+  };
+  auto tile_beg = [&](Pos c, Pos tb) -> uint32_t {  // column start relative to the tile, clamped to [0, TILE]
+    return c > tb ? (uint32_t)min(c - tb, (Pos)TILE) : 0u;
+  };
+  auto rows_issue = [&](int s, uint32_t t) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[s][e] = 0xFFFFFFFFu;
+    if (mcnt[s] > 32u) v[s][0] = kWide;
+    if (mcnt[s] == 0u || mcnt[s] > 32u) return;  // warp-uniform
+    const Pos tb = (Pos)t * TILE;
+    const uint32_t beg[1] = {tile_beg(crc[s], tb)};
+    const Pos base[1] = {(Pos)(cro[s] - crc[s])};
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const Pos g = tb + 32u * e + lane;
+      const Pos b = short_map<1, Pos>(beg, base, 32u * e, lane);
+      ld_stream_u32_if(g < tot, row + (Pos)(b + g), v[s][e]);  // Alg.3 line 4
+    }
+  };
+  auto test_red = [&](const uint32_t (&vv)[E]) {
+    uint32_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
+      BCHECK(vv[e] == 0xFFFFFFFFu || vv[e] < info->cap_nrows);
+      x[e] = probe_lean<SEG1>(vv[e], hw, sa, vis, bl, bmask);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) red_lean(x[e], vv[e], vis);  // Alg.3 line 7
+  };
+  // prologue: tables of tiles 0..2, columns of tiles 0..1, rows of tile 0
+  meta_load(0, t0);
+  meta_load(1, t0 + stride);
+  meta_load(2, t0 + 2 * stride);
+  cols_load(0);
+  cols_load(1);
+  rows_issue(0, t0);
+  for (uint32_t t = t0;;) {
+#pragma unroll
+    for (int p = 0; p < NS; ++p) {
+      if (t >= ntiles) return;  // warp-uniform
+      meta_load((p + 3) % NS, t + 3 * stride);  // ntiles + 3*stride < 2^32 (checked by the caller)
+      cols_load((p + 2) % NS);
+      rows_issue((p + 1) % NS, t + stride);
+      if (v[p][0] == kWide)  // warp-uniform
+        short_wide_tile<E, SEG1, POS32>(row, tile_k, rowoff_v, cumul_v, n, total, ntiles, t, vis, hw, sa, bl, bmask,
+                                        lane, info);
+      else test_red(v[p]);
+      t += stride;
+    }
+  }
+}
+
 
 template <int E, int THREADS, bool P1, bool SEG1, bool POS32>
 __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, const uint32_t* __restrict__ flist,
@@ -1125,6 +1373,14 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
   }
   // ---- short columns: tiles of TILE consecutive short edges, scan + binary-search mapping
   const ull ntiles = (total + TILE - 1) / TILE;
+  if constexpr (!P1 && BFS200_K1PIPE > 0 && BFS200_SHORTPIPE && E <= 4) {  // E = 8 would spill
+    if (ntiles + 4 * stride < (1ull << 32)) {  // tile ids stay 32-bit
+      short_tiles_p2<E, SEG1, POS32>(row, tile_k, rowoff_v, cumul_v, (uint32_t)n, total, (uint32_t)ntiles,
+                                     (uint32_t)((ull)blockIdx.x * WARPS + wid), (uint32_t)stride, vis, hw, sa, bl,
+                                     bmask, lane, info);
+      return;
+    }
+  }
   // software pipeline: the tile-table entries and the first 32 staged columns of the NEXT tile
   // are loaded while the current tile's row loads and visited tests are in flight.
   ull tile = (ull)blockIdx.x * WARPS + wid;
