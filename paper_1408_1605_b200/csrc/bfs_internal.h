@@ -76,6 +76,7 @@ struct Rank {
   uint64_t nz_rows = 0;  // local rows with at least one entry (for the parent-mode heuristic)
   unsigned long long* col = nullptr;  // [ncols+1] column offsets (u64: nnz can exceed 2^32)
   uint32_t* col32 = nullptr;          // [ncols+1] the same as u32 when nnz < 2^32 (read by K3)
+  uint8_t* deg8 = nullptr;            // [ncols] min(column degree, 255) (K3 count pass; 16-B aligned)
   uint32_t* row = nullptr;    // [nnz] local row ids, ascending within each column
   // CSR view of the same local matrix (row -> ascending local columns) for the parent pass;
   // with R = C = 1 the matrix is symmetric and these alias col/row.
@@ -105,7 +106,7 @@ struct Rank {
   unsigned long long* rowoff = nullptr;  // [ncols] col[flist[k]]
   unsigned long long* cumul = nullptr;   // [ncols+1] exclusive scan of degrees
   uint32_t* tile_k = nullptr;            // [nnz/32 + 2] first frontier index of every expansion tile
-  uint4* longlist = nullptr;             // [2 * (nnz/256 + 64)] hub columns (> 8 long tiles)
+  uint4* longlist = nullptr;             // [2 * (nnz/256 + nnz/32768 + 64)] hub entries (kernels.cu kHubChunk)
   void* seg_tot = nullptr;               // [nseg] per-segment totals (SegTot, kernels.cu)
   void* seg_off = nullptr;               // [nseg+1] K3 scratch: per-CTA totals of the count pass and their scan
   uint4* tileA = nullptr;                // [nnz/(TILE/2) + ncols] long-column tile records

@@ -129,6 +129,12 @@ __global__ void k_perm_from_sorted(const uint32_t* sorted, uint64_t n, uint32_t*
   }
 }
 
+// saturated column degrees for the K3 count pass: min(col[u+1] - col[u], 255)
+__global__ void k_deg8(const ull* col, uint64_t n, uint8_t* out) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    out[t] = (uint8_t)min(col[t + 1] - col[t], 255ull);
+}
+
 __global__ void k_narrow(const ull* in, uint64_t n, uint32_t* out) {
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
     out[t] = (uint32_t)in[t];
@@ -265,6 +271,10 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
     k_narrow<<<1024, 256, 0, s>>>(rk.col, nc, rk.col32);
     CKR(cudaGetLastError());
   }
+  rc = G_alloc(G, (void**)&rk.deg8, (g.ncols() + 32) * sizeof(uint8_t));  // ncols is a multiple of 32
+  if (rc) return rc;
+  k_deg8<<<1024, 256, 0, s>>>(rk.col, g.ncols(), rk.deg8);
+  CKR(cudaGetLastError());
   CKR(cudaStreamSynchronize(s));
   // CSR of the same local matrix for the parent pass (rows scanned in ascending ORIGINAL
   // column order; the CSC lists rows in relabeled order, so even a 1x1 grid needs its own copy)

@@ -204,7 +204,9 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.cumul, (g.ncols() + 1) * 8);
   AL(rk.tile_k, (rk.nnz / 32 + 2) * 4);          // short-edge tiles have >= 32 edges
   AL(rk.tileA, (3 * (rk.nnz / 32) + 64) * 16);    // long tiles: <= nnz/TILE + #long columns (d >= TILE/2)
-  AL(rk.longlist, 2 * (rk.nnz / 256 + 64) * 16);  // hub columns: > 8 tiles of >= 32 edges
+  // hub entries: <= one per column of > 8 tiles of >= 32 edges, + one per kHubChunk (1024) tiles
+  const uint64_t nhub = rk.nnz / 256 + rk.nnz / (32 * 1024) + 64;
+  AL(rk.longlist, 2 * nhub * 16);
   AL(rk.seg_tot, (nseg + 1) * 32);
   AL(rk.seg_off, (nseg + 8) * 32);  // CTA totals (nseg/8 + 1) and their scan (nseg/8 + 2)
   CKR(cudaMemsetAsync(rk.seg_tot, 0, (nseg + 1) * 32, G.stream));  // entry nseg stays zero
@@ -212,8 +214,7 @@ static int alloc_state(Graph& G, Rank& rk) {
   AL(rk.level_tmp, g.block * 4);
   AL(rk.scratch, 64 * 8);
   {  // array capacities for the bounds checks of a BFS200_CHECKS build (kernels.cu)
-    const unsigned long long caps[5] = {rk.nnz, g.ncols(), g.nrows(), 3 * (rk.nnz / 32) + 64,
-                                        2 * (rk.nnz / 256 + 64)};
+    const unsigned long long caps[5] = {rk.nnz, g.ncols(), g.nrows(), 3 * (rk.nnz / 32) + 64, 2 * nhub};
     CKR(cudaMemcpyAsync(&rk.info->cap_nnz, caps, sizeof caps, cudaMemcpyHostToDevice, G.stream));
   }
   if (g.C > 1) {

@@ -30,6 +30,9 @@ namespace bfs200 {
 typedef unsigned long long ull;
 
 // the pipelined short-tile loop of K1 in P2 levels (short_tiles_p2; 0 = the staged loop)
+#ifndef BFS200_EMIT_SMEM  // K3 emit pass: dense chunks' column offsets staged by async copies
+#define BFS200_EMIT_SMEM 1
+#endif
 #ifndef BFS200_SHORTPIPE
 #define BFS200_SHORTPIPE 1
 #endif
@@ -139,12 +142,14 @@ cudaError_t launch_init(const Geom& g, Rank& rk, bool owner, uint64_t root, bool
 struct SegTot {
   unsigned int cs;  // short columns
   unsigned int na;  // long-column tiles
-  unsigned int nh;  // hub columns (> 8 long tiles; their records are written by k_tile_fill)
+  unsigned int nh;  // hub entries: columns of > 8 long tiles, one entry per kHubChunk of their tiles (k_tile_fill)
   unsigned int pad;
   ull ss;           // short edges
   ull ls;           // long edges
 };
 static_assert(sizeof(SegTot) == 32, "engine.cu allocates 32 B per segment");
+constexpr unsigned kHubChunk = 1024;  // long tiles per hub entry (the records one k_tile_fill warp writes)
+__host__ __device__ constexpr unsigned hub_entries(unsigned nt) { return nt > 8 ? (nt + kHubChunk - 1) / kHubChunk : 0u; }
 #ifndef BFS200_BLIND3
 #define BFS200_BLIND3 1
 #endif
@@ -268,7 +273,8 @@ __global__ void __launch_bounds__(kSegScanThreads) k_seg_scan(const SegTot* __re
 }
 
 // Count pass: a warp owns a segment of kScanSegWords bitmap words; lane l takes word 32c + l of
-// chunk c and walks its set bits (the col[] pairs of one word share 8 sectors, cached in L1).
+// chunk c and walks its set bits, their degrees read from the saturated byte copy deg8 (a quarter
+// of the bytes of col32, read as whole 32-B runs: no dependent per-column loads).
 // Fused frontier update of a 1x1 graph (no exchange between K4 and K3): K2 does not run; the
 // count pass of the NEXT level takes the frontier as the rows discovered in the previous level,
 // f = vis & ~vold, writes it to the frontier bitmap (read by the emit pass and K4), advances
@@ -283,7 +289,8 @@ struct FusedUpd {
 
 template <typename Col, bool FUSED>
 __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uint64_t nwords, uint64_t seg,
-                                            const Col* __restrict__ col, int tile_shift, const FusedUpd& fu) {
+                                            const Col* __restrict__ col, const uint8_t* __restrict__ deg8,
+                                            int tile_shift, const FusedUpd& fu) {
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = seg * kScanSegWords;
   const uint64_t w1 = min(w0 + kScanSegWords, nwords);
@@ -322,68 +329,60 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
     }
     if (!__any_sync(0xFFFFFFFFu, any != 0u)) return SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
   }
-  __shared__ uint16_t s_lists[kScanThreads / 32][1024];
-  uint16_t* s_list = s_lists[threadIdx.x >> 5];
   auto add_col = [&](ull d) {
     if (d >= half) {
       const unsigned nt = (unsigned)((d + tm) >> tile_shift);
       t.na += nt;
-      t.nh += nt > 8 ? 1u : 0u;
+      t.nh += hub_entries(nt);
       t.ls += d;
     } else if (d) {
       t.cs += 1u;
       t.ss += d;
     }
   };
-#pragma unroll 1
-  for (int cw = 0; cw < kScanSegWords / 32; ++cw) {
-    const uint64_t wb = w0 + 32 * cw;
-    if (wb >= w1) break;  // warp-uniform
-    const uint64_t w = wb + lane;
-    uint32_t x = xw[0];  // xw[cw] without dynamic indexing (stays in registers)
+  // Lane l takes word w of chunk c (w = w0 + 32c + l) and the saturated degrees of its 32 columns,
+  // deg8[32w .. 32w + 32) (two 16-B loads; a warp reads 1 KB contiguous, two chunks in flight);
+  // the exact degree comes from col[] only for a saturated byte (degree >= 255).
+  auto add_word = [&](uint32_t x, const uint4& lo, const uint4& hi, uint64_t w) {
+    const uint32_t dw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t sat = 0;  // frontier columns of saturated degree (hubs): exact degree from col[]
 #pragma unroll
-    for (int c = 1; c < kScanSegWords / 32; ++c)
-      if (cw == c) x = xw[c];
-    const unsigned nbits = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(x));
-    if (nbits >= 96) {
-      // dense chunk: compact the set bits, then 32 consecutive frontier columns per step (their
-      // col[] entries share lines) -- the same order as k_scan_emit
-      const unsigned c = __popc(x);
-      unsigned incl = c;
-#pragma unroll
-      for (int s2 = 1; s2 < 32; s2 <<= 1) {
-        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, s2);
-        if (lane >= s2) incl += y;
+    for (int j = 0; j < 8; ++j) {
+      for (uint32_t bits = (x >> (4 * j)) & 0xFu; bits; bits &= bits - 1) {
+        const int bb = __ffs(bits) - 1;
+        const uint32_t d = (dw[j] >> (8 * bb)) & 0xFFu;
+        if (d == 255u) sat |= 1u << (4 * j + bb);
+        else add_col(d);
       }
-      unsigned p = incl - c;
-      for (uint32_t y = x; y; y &= y - 1) s_list[p++] = (uint16_t)(lane * 32 + __ffs(y) - 1);
-      __syncwarp();
-      for (unsigned g = 0; g < nbits; g += 64) {
-        ull dd[2];
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const unsigned idx = g + 32 * b + lane;
-          const uint64_t u = wb * 32 + (idx < nbits ? s_list[idx] : 0u);
-          dd[b] = idx < nbits ? (ull)(__ldg(col + u + 1) - __ldg(col + u)) : 0ull;
-        }
-        add_col(dd[0]);
-        add_col(dd[1]);
-      }
-      __syncwarp();
-      continue;
     }
-    while (x) {  // 4 set bits at a time: their col[] loads are in flight together
+    while (sat) {  // 4 at a time: their col[] loads in flight together (hub words of the first levels)
       ull dd[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int b = x ? __ffs(x) - 1 : -1;
-        x &= x ? x - 1 : 0u;
+        const int b = sat ? __ffs(sat) - 1 : -1;
+        sat &= sat ? sat - 1 : 0u;
         const uint64_t u = w * 32 + (b < 0 ? 0 : b);
         dd[q] = b < 0 ? 0ull : (ull)(__ldg(col + u + 1) - __ldg(col + u));
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) add_col(dd[q]);
     }
+  };
+  const uint4* __restrict__ d16 = reinterpret_cast<const uint4*>(deg8);
+#pragma unroll
+  for (int c = 0; c < kScanSegWords / 32; c += 2) {
+    uint4 dg[2][2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t w = w0 + 32 * (c + k) + lane;
+      dg[k][0] = dg[k][1] = make_uint4(0u, 0u, 0u, 0u);
+      if (xw[c + k]) {  // zero past w1
+        dg[k][0] = __ldg(d16 + 2 * w);
+        dg[k][1] = __ldg(d16 + 2 * w + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) add_word(xw[c + k], dg[k][0], dg[k][1], w0 + 32 * (c + k) + lane);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -402,13 +401,13 @@ __device__ __forceinline__ SegTot count_seg(const uint32_t* __restrict__ bm, uin
 template <typename Col, bool FUSED>
 __global__ void __launch_bounds__(kScanThreads) k_scan_count(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                               uint64_t nseg, const Col* __restrict__ col,
-                                                              SegTot* seg_tot, SegTot* cta_tot, int tile_shift,
-                                                              FusedUpd fu) {
+                                                              const uint8_t* __restrict__ deg8, SegTot* seg_tot,
+                                                              SegTot* cta_tot, int tile_shift, FusedUpd fu) {
   __shared__ SegTot s_t[kScanThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t seg = (uint64_t)blockIdx.x * (kScanThreads / 32) + wid;
   const SegTot t =
-      seg < nseg ? count_seg<Col, FUSED>(bm, nwords, seg, col, tile_shift, fu) : SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
+      seg < nseg ? count_seg<Col, FUSED>(bm, nwords, seg, col, deg8, tile_shift, fu) : SegTot{0u, 0u, 0u, 0u, 0ull, 0ull};
   if (lane == 0) {
     if (seg < nseg) seg_tot[seg] = t;
     s_t[wid] = t;
@@ -464,6 +463,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   unsigned nlongcols = 0;
   __shared__ uint16_t s_lists[kScanThreads / 32][1024];
   uint16_t* s_list = s_lists[threadIdx.x >> 5];
+  // NARROW: the column offsets of a dense chunk (1024 columns + the end), one slice per warp
+  constexpr bool kEmitSmem = NARROW && BFS200_EMIT_SMEM;
+  __shared__ __align__(16) uint32_t s_cols[kEmitSmem ? kScanThreads / 32 : 1][kEmitSmem ? 1024 : 4];
   // compact 8-byte long-tile records (position, length) in P2 levels of the pipelined loop (the
   // column is only needed by the P1 claims): half the record traffic of K3 and K1
   const bool compact = NARROW && BFS200_K1PIPE > 0 && info->mode == 2 && tile_shift <= 8;
@@ -477,10 +479,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         if (compact) reinterpret_cast<uint2*>(tileA)[pa + q] = make_uint2((uint32_t)pos, (uint32_t)len);
         else tileA[pa + q] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)len, (uint32_t)u);
       }
-    } else {  // hub column: its tiles are written by k_tile_fill
-      BCHECK(2 * hub + 1 < info->cap_long && c0 + d <= info->cap_nnz);
-      longlist[2 * hub] = make_uint4((uint32_t)pa, nt, (uint32_t)u, (uint32_t)(pa >> 32));
-      longlist[2 * hub + 1] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)d, (uint32_t)(d >> 32));
+    } else {  // hub column: its tiles are written by k_tile_fill, kHubChunk per entry
+      for (unsigned k = 0; k < hub_entries(nt); ++k) {
+        const ull q0 = (ull)k * kHubChunk, pk = pa + q0, ck = c0 + (q0 << tile_shift), dk = d - (q0 << tile_shift);
+        const unsigned nk = min(nt - (unsigned)q0, kHubChunk);
+        BCHECK(2 * (hub + k) + 1 < info->cap_long && c0 + d <= info->cap_nnz);
+        longlist[2 * (hub + k)] = make_uint4((uint32_t)pk, nk, (uint32_t)u, (uint32_t)(pk >> 32));
+        longlist[2 * (hub + k) + 1] = make_uint4((uint32_t)ck, (uint32_t)(ck >> 32), (uint32_t)dk, (uint32_t)(dk >> 32));
+      }
     }
   };
   for (uint64_t wb = w0; wb < w1; wb += 32) {
@@ -490,6 +496,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
     if (nbits >= 96) {
       // dense chunk: compact its set bits (column offsets in the chunk, ascending) into this
       // warp's shared list, then emit 32 frontier columns per step with every lane busy
+      // (NARROW: the chunk's 1025 column offsets are first copied into the warp's shared slice
+      // with 16-B asynchronous copies -- one round trip, overlapping the compaction -- so the
+      // steps read no global memory; else the col loads of two steps are in flight together)
+      const uint64_t cw1 = min(wb + 32, w1);  // the chunk's words are [wb, cw1)
+      if constexpr (kEmitSmem) {
+        uint32_t* s_c = s_cols[wid];
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_c);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t piece = 32u * k + lane;  // columns 4*piece .. 4*piece+3 of the chunk (word piece/8)
+          if (wb + piece / 8 < cw1)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + 16u * piece),
+                         "l"(col + wb * 32 + 4ull * piece));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      }
+      // the end offset of the chunk's last column
+      const uint32_t cend = kEmitSmem ? (uint32_t)__ldg(col + cw1 * 32) : 0u;
+      const unsigned ccols = (unsigned)(cw1 - wb) * 32;
       const unsigned c = __popc(x);
       unsigned incl = c;
 #pragma unroll
@@ -499,61 +524,77 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
       }
       unsigned p = incl - c;
       for (uint32_t y = x; y; y &= y - 1) s_list[p++] = (uint16_t)(lane * 32 + __ffs(y) - 1);
+      if constexpr (kEmitSmem) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       __syncwarp();
-      for (unsigned g = 0; g < nbits; g += 64) {
-        ull c0b[2], c1b[2];
-        uint64_t ub[2];
+      // one step: lane = frontier column u (c0, d) of the compacted list, valid = inside the list
+      auto emit_step = [&](uint64_t u, ull c0, ull d, bool valid) {
+        const bool isl = valid && d >= half;
+        const unsigned ds = (valid && !isl) ? (unsigned)d : 0u;  // short degree < TILE/2
+        const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
+        const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
+        const unsigned ne = hub_entries(na);
+        unsigned inc = ds, ia = na, ih = ne;  // inclusive warp scans
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {  // col loads of two groups in flight together
-          const unsigned idx = g + 32 * b + lane;
-          const bool valid = idx < nbits;
-          ub[b] = wb * 32 + (valid ? s_list[idx] : 0u);
-          c0b[b] = valid ? (ull)__ldg(col + ub[b]) : 0ull;
-          c1b[b] = valid ? (ull)__ldg(col + ub[b] + 1) : 0ull;
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+          const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
+          const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
+          const unsigned y3 = __shfl_up_sync(0xFFFFFFFFu, ih, s2);
+          if (lane >= s2) {
+            inc += y1;
+            ia += y2;
+            ih += y3;
+          }
         }
+        if (ds) {
+          const uint64_t pos = k + __popc(smask & lt);
+          const ull eb = e + inc - ds;
+          BCHECK(pos < info->cap_ncols && u < info->cap_ncols && c0 + ds <= info->cap_nnz);
+          if (need_flist) flist[pos] = (uint32_t)u;
+          rowoff[pos] = (Off)c0;
+          cumul[pos] = (Off)eb;
+          for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) {
+            BCHECK(t < info->cap_nnz / 32 + 2);
+            tile_k[t] = (uint32_t)pos;
+          }
+        }
+        if (isl) {
+          emit_long(u, c0, d, a + ia - na, na, h + ih - ne);
+          ++nlongcols;
+        }
+        k += __popc(smask);
+        h += __shfl_sync(0xFFFFFFFFu, ih, 31);
+        e += __shfl_sync(0xFFFFFFFFu, inc, 31);
+        a += __shfl_sync(0xFFFFFFFFu, ia, 31);
+      };
+      if constexpr (kEmitSmem) {
+        const uint32_t* s_c = s_cols[wid];
+        for (unsigned g = 0; g < nbits; g += 32) {
+          const unsigned idx = g + lane;
+          const bool valid = idx < nbits;
+          const unsigned off = valid ? s_list[idx] : 0u;
+          const uint32_t c0 = s_c[off], c1 = off + 1 < ccols ? s_c[off + 1] : cend;
+          emit_step(wb * 32 + off, (ull)c0, (ull)(c1 - c0), valid);
+        }
+      } else {
+        for (unsigned g = 0; g < nbits; g += 64) {
+          ull c0b[2], c1b[2];
+          uint64_t ub[2];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          if (g + 32 * b >= nbits) break;  // warp-uniform
-          const uint64_t u = ub[b];
-          const ull c0 = c0b[b], d = c1b[b] - c0b[b];
-          const bool isl = d >= half;
-          const unsigned ds = isl ? 0u : (unsigned)d;  // short degree < TILE/2
-          const unsigned na = isl ? (unsigned)((d + tm) >> tile_shift) : 0u;
-          const unsigned smask = __ballot_sync(0xFFFFFFFFu, ds != 0);
-          const unsigned hmask = __ballot_sync(0xFFFFFFFFu, na > 8);
-          unsigned inc = ds, ia = na;  // inclusive warp scans
+          for (int b = 0; b < 2; ++b) {  // col loads of two groups in flight together
+            const unsigned idx = g + 32 * b + lane;
+            const bool valid = idx < nbits;
+            ub[b] = wb * 32 + (valid ? s_list[idx] : 0u);
+            c0b[b] = valid ? (ull)__ldg(col + ub[b]) : 0ull;
+            c1b[b] = valid ? (ull)__ldg(col + ub[b] + 1) : 0ull;
+          }
 #pragma unroll
-          for (int s2 = 1; s2 < 32; s2 <<= 1) {
-            const unsigned y1 = __shfl_up_sync(0xFFFFFFFFu, inc, s2);
-            const unsigned y2 = __shfl_up_sync(0xFFFFFFFFu, ia, s2);
-            if (lane >= s2) {
-              inc += y1;
-              ia += y2;
-            }
+          for (int b = 0; b < 2; ++b) {
+            if (g + 32 * b >= nbits) break;  // warp-uniform
+            emit_step(ub[b], c0b[b], c1b[b] - c0b[b], g + 32 * b + lane < nbits);
           }
-          if (ds) {
-            const uint64_t pos = k + __popc(smask & lt);
-            const ull eb = e + inc - ds;
-            BCHECK(pos < info->cap_ncols && u < info->cap_ncols && c0 + ds <= info->cap_nnz);
-            if (need_flist) flist[pos] = (uint32_t)u;
-            rowoff[pos] = (Off)c0;
-            cumul[pos] = (Off)eb;
-            for (ull t = (eb + tm) >> tile_shift; (t << tile_shift) < eb + ds; ++t) {
-              BCHECK(t < info->cap_nnz / 32 + 2);
-              tile_k[t] = (uint32_t)pos;
-            }
-          }
-          if (isl) {
-            emit_long(u, c0, d, a + ia - na, na, h + __popc(hmask & lt));
-            ++nlongcols;
-          }
-          k += __popc(smask);
-          h += __popc(hmask);
-          e += __shfl_sync(0xFFFFFFFFu, inc, 31);
-          a += __shfl_sync(0xFFFFFFFFu, ia, 31);
         }
       }
-      __syncwarp();  // the list is rewritten by the next chunk
+      __syncwarp();  // the list (and the offsets) are rewritten by the next chunk
       continue;
     }
     // sparse chunk: lane totals of its word (4 set bits at a time)
@@ -574,7 +615,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         if (d >= half) {
           const unsigned nt = (unsigned)((d + tm) >> tile_shift);
           na += nt;
-          nh += nt > 8 ? 1u : 0u;
+          nh += hub_entries(nt);
         } else if (d) {
           cs += 1u;
           ss += d;
@@ -610,7 +651,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
         const unsigned nt = (unsigned)((d + tm) >> tile_shift);
         emit_long(u, c0, d, aa, nt, hh);
         aa += nt;
-        hh += nt > 8 ? 1u : 0u;
+        hh += hub_entries(nt);
         ++nlongcols;
       } else if (d) {
         BCHECK(kk < info->cap_ncols && u < info->cap_ncols && c0 + d <= info->cap_nnz);
@@ -635,7 +676,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
   if (lane == 0 && nlongcols) atomicAdd(&info->nlongcols, (ull)nlongcols);
 }
 
-// long-tile records of hub columns: one warp per column
+// long-tile records of hub columns: one warp per hub entry (a hub of more than kHubChunk tiles
+// is listed as several entries by k_scan_emit, so no warp writes more than kHubChunk records)
 __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4* tileA, int tile_shift, int narrow) {
   const int lane = threadIdx.x & 31;
   const bool compact = narrow && BFS200_K1PIPE > 0 && info->mode == 2 && tile_shift <= 8;  // as in k_scan_emit
@@ -645,6 +687,7 @@ __global__ void k_tile_fill(const uint4* longlist, const LevelInfo* info, uint4*
     const uint4 h = longlist[2 * r], b = longlist[2 * r + 1];
     const ull pa = (ull)h.x | ((ull)h.w << 32);
     const ull c0 = (ull)b.x | ((ull)b.y << 32), d = (ull)b.z | ((ull)b.w << 32);
+    BCHECK(h.y <= (uint32_t)kHubChunk);
     for (uint32_t q = lane; q < h.y; q += 32) {
       const ull pos = c0 + ((ull)q << tile_shift);
       const ull len = min(d - ((ull)q << tile_shift), tm + 1);
@@ -668,13 +711,13 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   const FusedUpd fu{rk.vis, rk.vold, rk.all_front, rk.level, ctrl};
   if (ctrl) {  // fused update (1x1): narrow or not
     if (narrow)
-      k_scan_count<uint32_t, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu);
+      k_scan_count<uint32_t, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, rk.deg8, st, ct, ts, fu);
     else
-      k_scan_count<ull, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu);
+      k_scan_count<ull, true><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.deg8, st, ct, ts, fu);
   } else if (narrow) {
-    k_scan_count<uint32_t, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, st, ct, ts, fu);
+    k_scan_count<uint32_t, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col32, rk.deg8, st, ct, ts, fu);
   } else {
-    k_scan_count<ull, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, ct, ts, fu);
+    k_scan_count<ull, false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, rk.deg8, st, ct, ts, fu);
   }
 
   // exclusive scan of the CTA totals (co[grid] = level total) + the level's counters
@@ -686,7 +729,7 @@ cudaError_t launch_scan(const Geom& g, Rank& rk, uint32_t tile_edges, bool narro
   else
     k_scan_emit<false><<<grid, kScanThreads, 0, s>>>(rk.all_front, nwords, nseg, rk.col, st, co, rk.flist, rk.rowoff,
                                                      rk.cumul, rk.tile_k, rk.tileA, ts, rk.longlist, rk.info);
-  k_tile_fill<<<g.nsm * 2, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts, narrow ? 1 : 0);
+  k_tile_fill<<<g.nsm * 8, 256, 0, s>>>(rk.longlist, rk.info, rk.tileA, ts, narrow ? 1 : 0);
   return cudaGetLastError();
 }
 
