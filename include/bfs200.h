@@ -92,8 +92,9 @@ typedef struct {
                            may reach bfs_run arbitrarily long after its peers; within a run a peer
                            that stops for ~17 s makes the run fail with BFS_ENCCL. */
   int debug_flags;      /* testing only; 0 in production.  BFS_DEBUG_POS64: the expansion stages
-                           64-bit row positions even when every position fits in 32 bits (the
-                           kernel variant otherwise used only when a rank holds >= 2^32 entries). */
+                           64-bit row positions and the parent pass reads the 64-bit CSR row
+                           offsets even when every position fits in 32 bits (the kernel variants
+                           otherwise used only when a rank holds >= 2^32 entries). */
 } bfs_opts;
 
 enum { BFS_DEBUG_POS64 = 1 };

@@ -81,6 +81,7 @@ struct Rank {
   // CSR view of the same local matrix (row -> ascending local columns) for the parent pass;
   // with R = C = 1 the matrix is symmetric and these alias col/row.
   unsigned long long* csr_ptr = nullptr;  // [nrows+1]
+  uint32_t* csr_ptr32 = nullptr;          // [nrows+1] the same as u32 when nnz < 2^32 (read by K4)
   uint32_t* csr_col = nullptr;            // [nnz]
   uint32_t* tdeg = nullptr;   // [block] input tuples whose source is the owned vertex (m_comp), ORIGINAL offsets
   // hot-prefix relabeling maps (build_graph.cu): owned offsets original <-> relabeled, and the

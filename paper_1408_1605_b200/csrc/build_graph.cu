@@ -297,6 +297,12 @@ static int csc_from_keys(Graph& G, Rank& rk, ull* keys, uint64_t n, int rbits, c
   const uint64_t nr = g.nrows() + 1;
   k_offsets<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(sorted, rk.nnz, cbits, g.nrows(), rk.csr_ptr);
   CKR(cudaGetLastError());
+  if (rk.nnz < (1ull << 32)) {  // 32-bit copy for the parent pass
+    rc = G_alloc(G, (void**)&rk.csr_ptr32, nr * sizeof(uint32_t));
+    if (rc) return rc;
+    k_narrow<<<1024, 256, 0, s>>>(rk.csr_ptr, nr, rk.csr_ptr32);
+    CKR(cudaGetLastError());
+  }
   CKR(cudaStreamSynchronize(s));
   return BFS_OK;
 }

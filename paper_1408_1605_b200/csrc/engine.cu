@@ -796,7 +796,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
     if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
     CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
     if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
-    CKR(launch_parent(g, rk, fused_of(G), s));
+    CKR(launch_parent(g, rk, fused_of(G), (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
     if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
     // barrier 1: every fold store has landed, and every rank is done reading its frontier bitmap
     // (K2's peer stores below overwrite it)
@@ -817,7 +817,7 @@ static int enqueue_level(Graph& G, bool use_cond, int nlev) {
   if (ev && (rc = ev_rec(G, nlev, 2))) return rc;
   for (Rank& rk : G.ranks) CKR(launch_expand(g, rk, E, G.hot_h, (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
   if (ev && (rc = ev_rec(G, nlev, 3))) return rc;
-  for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, fused_of(G), s));
+  for (Rank& rk : G.ranks) CKR(launch_parent(g, rk, fused_of(G), (G.opts.debug_flags & BFS_DEBUG_POS64) != 0, s));
   if (ev && (rc = ev_rec(G, nlev, 4))) return rc;
   if ((rc = xl ? fold_exchange_x(G) : fold_exchange(G))) return rc;
   if (ev && (rc = ev_rec(G, nlev, 5))) return rc;

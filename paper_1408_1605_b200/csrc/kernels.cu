@@ -1679,9 +1679,12 @@ constexpr int kLaneStep = BFS200_LANE_STEP;  // CSR entries per lane step (loads
 constexpr int kParRows = BFS200_PAR_ROWS;  // P2 rows scanned together per lane
 constexpr size_t kParentHotSmem = 64 * 1024;  // hot prefix of the frontier bitmap (P2 levels)
 
+// Ptr: the CSR row offsets, the 32-bit copy when nnz < 2^32 (half the pointer bytes: every
+// discovered row of a P2 level reads its pair)
+template <typename Ptr>
 __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, const uint32_t* __restrict__ vold,
                                                                uint64_t nwords,
-                                                               const ull* __restrict__ csr_ptr,
+                                                               const Ptr* __restrict__ csr_ptr,
                                                                const uint32_t* __restrict__ csr_col,
                                                                const uint32_t* __restrict__ front, uint32_t* pred,
                                                                uint32_t* pmin, uint32_t* sendbuf,
@@ -1798,7 +1801,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
 #pragma unroll
         for (int i = 0; i < kParRows; ++i) {
           const bool v = r[i] != 0xFFFFFFFFu;
-          const ull beg = v ? csr_ptr[r[i]] : 0ull, end = v ? csr_ptr[r[i] + 1] : 0ull;
+          const ull beg = v ? (ull)csr_ptr[r[i]] : 0ull, end = v ? (ull)csr_ptr[r[i] + 1] : 0ull;
           p[i] = beg;
           stop[i] = min(end, beg + kShortScan);
           best[i] = 0xFFFFFFFFu;
@@ -1853,9 +1856,9 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
           const int src = __ffs(has) - 1;
           has &= has - 1;
           const uint32_t r = queue[wid][src + 32 * k];
-          const ull end = csr_ptr[r + 1];
+          const ull end = (ull)csr_ptr[r + 1];
           uint32_t best = 0xFFFFFFFFu;
-          for (ull p = csr_ptr[r] + kShortScan; p < end; p += 32) {
+          for (ull p = (ull)csr_ptr[r] + kShortScan; p < end; p += 32) {
             const uint32_t u = (p + lane < end) ? __ldg(csr_col + p + lane) : 0xFFFFFFFFu;
             const bool f = (u != 0xFFFFFFFFu) && in_front(u);
             const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
@@ -1916,7 +1919,7 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
   }
 }
 
-cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, cudaStream_t s) {
+cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, bool force_ptr64, cudaStream_t s) {
   const uint64_t nwords = g.nrows() / 32;
   const uint64_t nchunks = (nwords + 31) / 32;
   uint64_t grid = (nchunks + kParentThreads / 32 - 1) / (kParentThreads / 32);
@@ -1931,10 +1934,16 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, cudaStream_t s) {
   if (hw > g.words_block()) hw = g.words_block();
   if (blog < 0) hw = 0;
   const size_t smem = (size_t)(kParentThreads / 32) * 1024 * 4 + (size_t)(g.R * hw > 4 ? g.R * hw : 4) * 4;
-  k_parent<<<(unsigned)grid, kParentThreads, smem, s>>>(rk.vis, rk.vold, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred,
-                                                        rk.pmin, g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info,
-                                                        (uint32_t)hw, g.R, g.words_block(), blog,
-                                                        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
+  if (rk.csr_ptr32 && !force_ptr64)
+    k_parent<uint32_t><<<(unsigned)grid, kParentThreads, smem, s>>>(
+        rk.vis, rk.vold, nwords, rk.csr_ptr32, rk.csr_col, rk.all_front, rk.pred, rk.pmin,
+        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog,
+        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
+  else
+    k_parent<ull><<<(unsigned)grid, kParentThreads, smem, s>>>(
+        rk.vis, rk.vold, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred, rk.pmin,
+        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog,
+        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -1948,7 +1957,9 @@ cudaError_t kernels_init_device() {
   if (e == cudaSuccess) e = expand_attrs<8, 1024>();
   if (e == cudaSuccess) e = expand_attrs<16, 512>();
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    e = cudaFuncSetAttribute(k_parent<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_parent<ull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
   return e;
 }
 

@@ -27,7 +27,7 @@ cudaError_t launch_expand(const Geom& g, Rank& rk, int edges_per_thread, uint64_
 uint32_t expand_tile_edges(int edges_per_thread);
 
 // K4: parent claim for the rows discovered in this level (+ pack of the fold message, C > 1).
-cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, cudaStream_t s);
+cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, bool force_ptr64, cudaStream_t s);
 
 // K2: frontier update + pack; lvl is the level being assigned.
 cudaError_t launch_update(const Geom& g, Rank& rk, const LevelCtrl* ctrl, cudaStream_t s);
