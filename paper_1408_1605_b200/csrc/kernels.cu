@@ -30,6 +30,9 @@ namespace bfs200 {
 typedef unsigned long long ull;
 
 // the pipelined short-tile loop of K1 in P2 levels (short_tiles_p2; 0 = the staged loop)
+#ifndef BFS200_K1AHEAD  // long_tiles_p2: tiles whose rows are in flight ahead of the one tested
+#define BFS200_K1AHEAD (BFS200_K1PIPE - 1)
+#endif
 #ifndef BFS200_EMIT_SMEM  // K3 emit pass: dense chunks' column offsets staged by async copies
 #define BFS200_EMIT_SMEM 1
 #endif
@@ -887,183 +890,26 @@ __device__ __forceinline__ void expand_edges(const uint32_t (&v)[WV], const uint
 }
 
 // Long-column tiles of a P2 level, software-pipelined (the hot loop of the peak level).  A warp
-// walks its tiles q = 0, 1, ... (tile id t0 + q*stride) through NS row slots.  Phase q: the
-// `row` loads of tile q+NS-1 (into the slot tile q-1 freed), the record of tile q+2NS-1 (NS
-// phases ahead), then the visited tests of tile q -- hot copy in shared memory, else one L2 probe
-// of the visited|discovered pair -- and its RED.ORs (Alg.3 lines 4-7).  So every tile's rows have
-// NS-1 phases to arrive from HBM and no phase waits for a record.  Slots are compile-time indices
-// of a loop unrolled NS times (no register moves between slots: a moved register waits for its
-// load).  A row id of 0xFFFFFFFF marks a lane past the tile's end (partial last tile of a column,
-// or past the warp's last tile).  Not inlined: its registers are allocated apart from the rest of
-// k_expand (inlined, the short-tile state live across it made both spill).
-// Measured at s26, peak level (tools/ab_expand.py, same box, two runs each): the previous
-// double-buffered loop 3.19 ms; this loop with NS = 2 / 3 / 4: 3.20 / 3.08 / 4.24 ms (NS = 4
-// spills); the REDs deferred one phase behind the next tile's probes: 3.34 ms (NS = 2); a
-// warp-uniform full-tile branch without per-lane bounds: 3.46 ms; a probe returning x = ~0 instead
-// of a need flag: 3.17 ms.
-// Register-lean forms of probe_seg1 / probe_segs / probe_red for the pipelined loop: the probe
-// keeps only the loaded pair (x, y) and the need flag; the RED recomputes the row's bit mask and
-// word address from v (two instructions instead of three live registers per row).
-// Probe and RED of one row of a long tile (the hot loop of the peak level): the probe returns the
-// loaded visited word, the need flag, the row's bit mask and its word address, and the RED reuses
-// them; the lane's validity is the row sentinel (0xFFFFFFFF past a tile's end).
-__device__ __forceinline__ void probe4_seg1(uint32_t& x, uint32_t& need, uint32_t& m, uint32_t*& a, uint32_t v,
-                                            uint32_t hw, uint32_t sa, uint32_t* vis) {
-  asm("{\n"
-      " .reg .pred pok, pn;\n"
-      " .reg .b32 wi, hi, hv;\n"
-      " setp.ne.u32 pok, %4, 0xFFFFFFFF;\n"
-      " shr.b32 wi, %4, 5;\n"
-      " min.u32 hi, wi, %5;\n"
-      " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %6;\n"
-      " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
-      " and.b32 hv, hv, %2;\n"
-      " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 %3, wi, 4, %7;\n"
-      " @pn ld.global.cg.u32 %0, [%3];\n"
-      " selp.u32 %1, 1, 0, pn;\n"
-      "}"
-      : "=r"(x), "=r"(need), "=r"(m), "=l"(a)
-      : "r"(v), "r"(hw), "r"(sa), "l"(vis));
-}
-__device__ __forceinline__ void probe4_segs(uint32_t& x, uint32_t& need, uint32_t& m, uint32_t*& a, uint32_t v,
-                                            uint32_t hw, uint32_t sa, uint32_t* vis, int bl, uint32_t bmask) {
-  asm("{\n"
-      " .reg .pred pok, pn;\n"
-      " .reg .b32 wi, hi, hv, sg, off;\n"
-      " setp.ne.u32 pok, %4, 0xFFFFFFFF;\n"
-      " shr.b32 wi, %4, 5;\n"
-      " shr.b32 sg, %4, %8;\n"
-      " and.b32 off, %4, %9;\n"
-      " shr.b32 off, off, 5;\n"
-      " min.u32 off, off, %5;\n"
-      " add.u32 hv, %5, 1;\n"
-      " mad.lo.u32 hi, sg, hv, off;\n"
-      " selp.u32 hi, hi, %5, pok;\n"
-      " shl.b32 hi, hi, 2;\n"
-      " add.u32 hi, hi, %6;\n"
-      " ld.shared.u32 hv, [hi];\n"
-      " shf.l.wrap.b32 %2, 0, 1, %4;\n"
-      " and.b32 hv, hv, %2;\n"
-      " setp.eq.and.b32 pn, hv, 0, pok;\n"
-      " mad.wide.u32 %3, wi, 4, %7;\n"
-      " @pn ld.global.cg.u32 %0, [%3];\n"
-      " selp.u32 %1, 1, 0, pn;\n"
-      "}"
-      : "=r"(x), "=r"(need), "=r"(m), "=l"(a)
-      : "r"(v), "r"(hw), "r"(sa), "l"(vis), "r"(bl), "r"(bmask));
-}
-__device__ __forceinline__ void red4(uint32_t x, uint32_t need, uint32_t m, uint32_t* a) {
-  asm volatile("{\n"
-               " .reg .pred pn, pr;\n"
-               " .reg .b32 t;\n"
-               " setp.ne.b32 pn, %1, 0;\n"
-               " and.b32 t, %0, %2;\n"
-               " setp.eq.and.b32 pr, t, 0, pn;\n"
-               " @pr red.relaxed.gpu.global.or.b32 [%3], %2;\n"
-               "}" ::"r"(x), "r"(need), "r"(m), "l"(a));
-}
-
-template <int E, bool SEG1, bool POS32, int NS>
-__device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
-                                           uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vis, uint32_t hw,
-                                           uint32_t sa, int bl, uint32_t bmask, int lane, const LevelInfo* info) {
-  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
-  uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
-  Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
-  uint32_t rlen[NS];
-  auto rec_load = [&](int slot, uint32_t t) {
-    rlen[slot] = 0u;
-    rpos[slot] = 0;
-    if (t < nA) {
-      if (POS32) {  // compact records (k_scan_emit: narrow, P2, E <= 8)
-        const uint2 r = reinterpret_cast<const uint2*>(tileA)[t];
-        BCHECK((ull)r.x + r.y <= info->cap_nnz && r.y <= 32u * E);
-        rpos[slot] = (Pos)r.x;
-        rlen[slot] = r.y;
-      } else {
-        const uint4 r = tileA[t];
-        BCHECK(((ull)r.x | ((ull)r.y << 32)) + r.z <= info->cap_nnz && r.z <= 32u * E);
-        rpos[slot] = (Pos)((ull)r.x | ((ull)r.y << 32));
-        rlen[slot] = r.z;
-      }
-    }
-  };
-  auto rows_issue = [&](int slot) {  // from the record in the same slot
-    const uint32_t* rp = row + rpos[slot] + lane;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      v[slot][e] = 0xFFFFFFFFu;
-      ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);  // Alg.3 line 4
-    }
-  };
-  // prologue: rows of tiles 0 .. NS-2 issued; records of tiles NS-1 .. 2NS-2 prefetched
-  // (the warp's tile q is t0 + q*stride; tile ids and counts fit in 32 bits: tileA holds < 2^32)
-#pragma unroll
-  for (int k = 0; k < NS - 1; ++k) {
-    rec_load(k, t0 + (uint32_t)k * stride);
-    rows_issue(k);
-  }
-#pragma unroll
-  for (int k = 0; k < NS - 1; ++k) rec_load(k, t0 + (uint32_t)(NS + k) * stride);
-  rec_load(NS - 1, t0 + (uint32_t)(NS - 1) * stride);
-  const uint32_t ahead = (uint32_t)(2 * NS - 1) * stride;
-  for (uint32_t t = t0;;) {
-#pragma unroll
-    for (int p = 0; p < NS; ++p) {
-      if (t >= nA) return;  // warp-uniform
-      const int sn = (p + NS - 1) % NS;  // slot of tile q+NS-1 (its record is loaded)
-      rows_issue(sn);
-      rec_load(sn, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
-      uint32_t x[E], need[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) BCHECK(v[p][e] == 0xFFFFFFFFu || v[p][e] < info->cap_nrows);
-      uint32_t mk[E];
-      uint32_t* ad[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
-        if (SEG1) probe4_seg1(x[e], need[e], mk[e], ad[e], v[p][e], hw, sa, vis);
-        else probe4_segs(x[e], need[e], mk[e], ad[e], v[p][e], hw, sa, vis, bl, bmask);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) red4(x[e], need[e], mk[e], ad[e]);  // Alg.3 line 7
-      t += stride;
-    }
-  }
-}
-
-// Edge -> column mapping of one 32-edge window of a short tile, in registers (the paper's
-// binary search of the scan, P:455-470 / Alg.3 line 2).  Lane l holds CS of the tile's columns,
-// l + 32c: beg = the column's first edge relative to the tile (0 for a column begun in an
-// earlier tile; TILE for lanes past the tile's last column) and base = its row offset minus its
-// scan value (row position of short edge g of the column = base + g, modular when Pos is 32-bit).
-// Columns have distinct starts (a short column has degree >= 1), so edge lo + lane belongs to
-// column k = #(columns starting before the window) + #(columns starting in the window at or
-// before the edge) - 1: one ballot and one OR-reduction of start bits per column set, a popcount,
-// then a shuffle of base from the lane holding column k.
-template <int CS, typename Pos>
-__device__ __forceinline__ Pos short_map(const uint32_t (&beg)[CS], const Pos (&base)[CS], uint32_t lo, int lane) {
-  uint32_t sb = 0, before = 0;
-#pragma unroll
-  for (int c = 0; c < CS; ++c) {
-    const uint32_t r = beg[c] - lo;  // in the window when r < 32 (unsigned)
-    sb |= __reduce_or_sync(0xFFFFFFFFu, r < 32u ? 1u << r : 0u);
-    before += __popc(__ballot_sync(0xFFFFFFFFu, beg[c] < lo));
-  }
-  const uint32_t k = before + __popc(sb & (0xFFFFFFFFu >> (31 - lane))) - 1u;
-  Pos b = __shfl_sync(0xFFFFFFFFu, base[0], (int)(k & 31u));
-#pragma unroll
-  for (int c = 1; c < CS; ++c) {
-    const Pos bc = __shfl_sync(0xFFFFFFFFu, base[c], (int)(k & 31u));
-    b = (k >> 5) == (uint32_t)c ? bc : b;
-  }
-  return b;
-}
-
-// Register-lean probe / RED for the short-tile loop (its pipeline state leaves no room for
-// probe4's mask and address): the probe leaves x = 0xFFFFFFFF when no RED is due (hot and
+// walks its tiles q = 0, 1, ... (tile id t0 + q*stride) through NS register slots.  Phase q: the
+// `row` loads of tile q+AHEAD (into a slot already tested and RED'ed), the record of tile
+// q+AHEAD+NS, then the visited tests of tile q -- hot copy in shared memory, else one L2 probe of
+// the visited word -- and the RED.ORs of tile q (Alg.3 lines 4-7).  So every tile's rows have AHEAD phases to arrive from
+// HBM and no phase waits for a record.  Slots are compile-time indices of a loop unrolled NS times
+// (no register moves between slots: a moved register waits for its load).  A row id of 0xFFFFFFFF
+// marks a lane past the tile's end (partial last tile of a column, or past the warp's last tile).
+// The probe keeps one register per row (probe_lean: the loaded word, 0xFFFFFFFF when no RED is
+// due; the RED recomputes bit and address from the row id).  Not inlined: its registers are
+// allocated apart from the rest of k_expand (inlined, the short-tile state live across it made
+// both spill).
+// Measured at s26, peak level (tools/ab_expand.py, same box, two runs each): the round-1
+// double-buffered loop 3.19 ms; this loop with NS = 2 / 3 / 4 (AHEAD = NS-1) and a probe keeping
+// the need flag, mask and address (5 registers per row): 3.20 / 3.08 / 4.24 ms (NS = 4 spills);
+// the REDs deferred (NS = 2): 3.34 ms; a warp-uniform full-tile branch without per-lane bounds:
+// 3.46 ms.  Later (profiles/r02_long_lean_ab.log): the lean probe at NS = 3 / 4 / 5 (AHEAD =
+// NS-1): 2.78 → 2.69 / 2.69 / 2.83 ms per peak level; the REDs of tile q deferred behind tile
+// q+1's probes (one more slot of rows and probed words) spill at NS = 4 and 5 (not measured).
+// Register-lean probe / RED for the pipelined loops (no room for a need flag, mask and address
+// per row next to their pipeline state): the probe leaves x = 0xFFFFFFFF when no RED is due (hot and
 // visited, or no row), else the loaded visited word; the RED recomputes the bit and the word
 // address from v.  Two live registers per row instead of five.
 template <bool SEG1>
@@ -1131,6 +977,103 @@ __device__ __forceinline__ void red_lean(uint32_t x, uint32_t v, uint32_t* vis) 
                " mad.wide.u32 a, wi, 4, %2;\n"
                " @pr red.relaxed.gpu.global.or.b32 [a], m;\n"
                "}" ::"r"(x), "r"(v), "l"(vis));
+}
+
+template <int E, bool SEG1, bool POS32, int NS, int AHEAD>
+__device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, const uint4* __restrict__ tileA,
+                                           uint32_t nA, uint32_t t0, uint32_t stride, uint32_t* vis, uint32_t hw,
+                                           uint32_t sa, int bl, uint32_t bmask, int lane, const LevelInfo* info) {
+  static_assert(AHEAD >= 1 && AHEAD <= NS - 1, "row slots: AHEAD tiles in flight + the tested one");
+  typedef typename std::conditional<POS32, uint32_t, ull>::type Pos;
+  uint32_t v[NS][E];  // row ids of the tiles in flight; 0xFFFFFFFF past a tile's end
+  uint32_t x[NS][E];  // probed visited words (probe_lean; 0xFFFFFFFF: no RED due)
+  Pos rpos[NS];       // prefetched records: position, length (0 past the warp's last tile)
+  uint32_t rlen[NS];
+  auto rec_load = [&](int slot, uint32_t t) {
+    rlen[slot] = 0u;
+    rpos[slot] = 0;
+    if (t < nA) {
+      if (POS32) {  // compact records (k_scan_emit: narrow, P2, E <= 8)
+        const uint2 r = reinterpret_cast<const uint2*>(tileA)[t];
+        BCHECK((ull)r.x + r.y <= info->cap_nnz && r.y <= 32u * E);
+        rpos[slot] = (Pos)r.x;
+        rlen[slot] = r.y;
+      } else {
+        const uint4 r = tileA[t];
+        BCHECK(((ull)r.x | ((ull)r.y << 32)) + r.z <= info->cap_nnz && r.z <= 32u * E);
+        rpos[slot] = (Pos)((ull)r.x | ((ull)r.y << 32));
+        rlen[slot] = r.z;
+      }
+    }
+  };
+  auto rows_issue = [&](int slot) {  // from the record in the same slot
+    const uint32_t* rp = row + rpos[slot] + lane;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      v[slot][e] = 0xFFFFFFFFu;
+      ld_stream_u32_if(32u * e + lane < rlen[slot], rp + 32 * e, v[slot][e]);  // Alg.3 line 4
+    }
+  };
+  auto reds = [&](int slot) {  // Alg.3 line 7
+#pragma unroll
+    for (int e = 0; e < E; ++e) red_lean(x[slot][e], v[slot][e], vis);
+  };
+  // prologue: rows of tiles 0 .. AHEAD-1 issued; records of tiles AHEAD .. AHEAD+NS-1 prefetched
+  // (the warp's tile q is t0 + q*stride; tile ids and counts fit in 32 bits: tileA holds < 2^32)
+#pragma unroll
+  for (int k = 0; k < AHEAD; ++k) {
+    rec_load(k, t0 + (uint32_t)k * stride);
+    rows_issue(k);
+  }
+#pragma unroll
+  for (int k = AHEAD; k < NS; ++k) rec_load(k, t0 + (uint32_t)k * stride);
+#pragma unroll
+  for (int k = 0; k < AHEAD; ++k) rec_load(k, t0 + (uint32_t)(NS + k) * stride);
+  const uint32_t ahead = (uint32_t)(AHEAD + NS) * stride;
+  for (uint32_t t = t0;;) {
+#pragma unroll
+    for (int p = 0; p < NS; ++p) {
+      if (t >= nA) return;  // warp-uniform
+      const int sr = (p + AHEAD) % NS;  // slot of tile q+AHEAD (its record is loaded)
+      rows_issue(sr);
+      rec_load(sr, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
+#pragma unroll
+      for (int e = 0; e < E; ++e) {  // Alg.3 lines 5-6
+        BCHECK(v[p][e] == 0xFFFFFFFFu || v[p][e] < info->cap_nrows);
+        x[p][e] = probe_lean<SEG1>(v[p][e], hw, sa, vis, bl, bmask);
+      }
+      reds(p);
+      t += stride;
+    }
+  }
+}
+
+// Edge -> column mapping of one 32-edge window of a short tile, in registers (the paper's
+// binary search of the scan, P:455-470 / Alg.3 line 2).  Lane l holds CS of the tile's columns,
+// l + 32c: beg = the column's first edge relative to the tile (0 for a column begun in an
+// earlier tile; TILE for lanes past the tile's last column) and base = its row offset minus its
+// scan value (row position of short edge g of the column = base + g, modular when Pos is 32-bit).
+// Columns have distinct starts (a short column has degree >= 1), so edge lo + lane belongs to
+// column k = #(columns starting before the window) + #(columns starting in the window at or
+// before the edge) - 1: one ballot and one OR-reduction of start bits per column set, a popcount,
+// then a shuffle of base from the lane holding column k.
+template <int CS, typename Pos>
+__device__ __forceinline__ Pos short_map(const uint32_t (&beg)[CS], const Pos (&base)[CS], uint32_t lo, int lane) {
+  uint32_t sb = 0, before = 0;
+#pragma unroll
+  for (int c = 0; c < CS; ++c) {
+    const uint32_t r = beg[c] - lo;  // in the window when r < 32 (unsigned)
+    sb |= __reduce_or_sync(0xFFFFFFFFu, r < 32u ? 1u << r : 0u);
+    before += __popc(__ballot_sync(0xFFFFFFFFu, beg[c] < lo));
+  }
+  const uint32_t k = before + __popc(sb & (0xFFFFFFFFu >> (31 - lane))) - 1u;
+  Pos b = __shfl_sync(0xFFFFFFFFu, base[0], (int)(k & 31u));
+#pragma unroll
+  for (int c = 1; c < CS; ++c) {
+    const Pos bc = __shfl_sync(0xFFFFFFFFu, base[c], (int)(k & 31u));
+    b = (k >> 5) == (uint32_t)c ? bc : b;
+  }
+  return b;
 }
 
 // One short tile of more than 32 columns (runs of degree-1..3 columns) of a P2 level: its table
@@ -1374,8 +1317,8 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
     if constexpr (!P1 && BFS200_K1PIPE > 0 && E <= 8) {
-      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE>(row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vis, hw, sa,
-                                                    bl, bmask, lane, info);
+      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE, BFS200_K1AHEAD>(
+          row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vis, hw, sa, bl, bmask, lane, info);
     } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);
     ull t1 = t + stride;

@@ -21,7 +21,7 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 BUILD = {"k_count", "k_scatter", "k_kron_generate", "k_keys_to_rows", "k_keys_to_cols", "k_csr_keys", "k_offsets",
-         "k_slice", "k_degree_keys", "k_iota2", "k_apply_moves", "k_count_nz_rows", "k_perm_from_sorted", "k_narrow"}
+         "k_slice", "k_degree_keys", "k_iota2", "k_apply_moves", "k_count_nz_rows", "k_perm_from_sorted", "k_narrow", "k_deg8"}
 
 
 def launch_summary(path):
