@@ -122,7 +122,7 @@ struct Rank {
   void* scan_tmp = nullptr;      // CUB temp for the popcount scans
   size_t scan_tmp_bytes = 0;
   uint32_t* resp = nullptr;      // [nrows] compacted responses (sent)
-  uint32_t* respin = nullptr;    // [nrows] compacted responses (received)
+  uint32_t* respin = nullptr;    // [nrows] segment c: column c's answers (compacted; peer exchange: by owned offset)
   // list exchange (opts.exchange != 0), allocated on first use; S = max(R, C) segments of W words
   uint32_t* xsend = nullptr;     // [S*W] outgoing index lists, segment k at k*W
   uint32_t* xrecv = nullptr;     // [S*W] incoming index lists
@@ -133,8 +133,7 @@ struct Rank {
   // peer exchange (opts.peer_exchange): device arrays of peer pointers, null when inactive
   uint32_t** fold_dst = nullptr;  // [C] recv of P_ic + j*W (null for c == j)
   uint32_t** exp_dst = nullptr;   // [R] all_front of P_(i2)j + i*W (null for i2 == i)
-  uint32_t** reqin_dst = nullptr;   // [C] reqin of P_ic + j*W (null for c == j)
-  uint32_t** respin_dst = nullptr;  // [C] respin of P_ic + j*block (null for c == j)
+  uint32_t** respin_dst = nullptr;  // [C] respin of P_ic + j*block (null for c == j): K4's parent candidates
   unsigned long long* scratch = nullptr;  // small reduction scratch
 };
 

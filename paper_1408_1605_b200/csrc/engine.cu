@@ -420,15 +420,14 @@ static int setup_peer(Graph& G) {
   if ((rc = G_alloc(G, (void**)&G.d_xerr, 8))) return rc;
   // C == 1: no fold / resolution buffers; dummies keep the handle layout uniform
   if (!rk.recv && (rc = G_alloc(G, (void**)&rk.recv, 16))) return rc;
-  if (!rk.reqin && (rc = G_alloc(G, (void**)&rk.reqin, 16))) return rc;
   if (!rk.respin && (rc = G_alloc(G, (void**)&rk.respin, 16))) return rc;
   CKR(cudaMemset(G.xsig, 0, 64 * sizeof(XSig)));
   CKR(cudaMemset(G.d_epoch, 0, 8));
   CKR(cudaMemset(G.d_xerr, 0, 8));
-  constexpr int NH = 5;
+  constexpr int NH = 4;
   cudaIpcMemHandle_t mine[NH];
   memset(mine, 0, sizeof mine);
-  void* const bufs[NH] = {rk.recv, rk.all_front, G.xsig, rk.reqin, rk.respin};
+  void* const bufs[NH] = {rk.recv, rk.all_front, G.xsig, rk.respin};
   for (int k = 0; k < NH && !local_fail; ++k) {
     const cudaError_t e = cudaIpcGetMemHandle(&mine[k], bufs[k]);
     if (e != cudaSuccess) fail("peer_exchange: cudaIpcGetMemHandle", e);
@@ -467,15 +466,13 @@ static int setup_peer(Graph& G) {
       return set_err(BFS_ECUDA, "%s", local_fail ? why.c_str() : "peer_exchange: setup failed on another rank");
     }
   }
-  const std::vector<void*>&recv_of = of[0], &front_of = of[1], &sig_of = of[2], &reqin_of = of[3],
-                            &respin_of = of[4];
-  // tables: fold_dst[c] = recv of P_ic + j*W; exp_dst[i2] = all_front of P_(i2)j + i*W
-  std::vector<uint32_t*> fold((size_t)g.C, nullptr), expd((size_t)g.R, nullptr), rqd((size_t)g.C, nullptr),
-      rsd((size_t)g.C, nullptr);
+  const std::vector<void*>&recv_of = of[0], &front_of = of[1], &sig_of = of[2], &respin_of = of[3];
+  // tables: fold_dst[c] = recv of P_ic + j*W; exp_dst[i2] = all_front of P_(i2)j + i*W;
+  // respin_dst[c] = respin of P_ic + j*block (K4's parent candidates for the rows P_ic owns)
+  std::vector<uint32_t*> fold((size_t)g.C, nullptr), expd((size_t)g.R, nullptr), rsd((size_t)g.C, nullptr);
   for (int c = 0; c < g.C; ++c)
     if (c != rk.j) {
       fold[c] = static_cast<uint32_t*>(recv_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
-      rqd[c] = static_cast<uint32_t*>(reqin_of[c * g.R + rk.i]) + (uint64_t)rk.j * W;
       rsd[c] = static_cast<uint32_t*>(respin_of[c * g.R + rk.i]) + (uint64_t)rk.j * g.block;
     }
   for (int i2 = 0; i2 < g.R; ++i2)
@@ -487,9 +484,7 @@ static int setup_peer(Graph& G) {
   if ((rc = G_alloc(G, (void**)&G.d_sig_peers, P * sizeof(XSig*)))) return rc;
   CKR(cudaMemcpy(rk.fold_dst, fold.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
   CKR(cudaMemcpy(rk.exp_dst, expd.data(), g.R * sizeof(uint32_t*), cudaMemcpyHostToDevice));
-  if ((rc = G_alloc(G, (void**)&rk.reqin_dst, g.C * sizeof(uint32_t*)))) return rc;
   if ((rc = G_alloc(G, (void**)&rk.respin_dst, g.C * sizeof(uint32_t*)))) return rc;
-  CKR(cudaMemcpy(rk.reqin_dst, rqd.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
   CKR(cudaMemcpy(rk.respin_dst, rsd.data(), g.C * sizeof(uint32_t*), cudaMemcpyHostToDevice));
   CKR(cudaMemcpy(G.d_sig_peers, sigs.data(), P * sizeof(XSig*), cudaMemcpyHostToDevice));
   // the peers' arrays must be zero (epochs start at 0) before anyone signals
@@ -693,17 +688,10 @@ static int resolve_parents(Graph& G) {
   const uint64_t W = g.words_block();
   const int C = g.C;
   cudaStream_t s = G.stream;
-  if (peer_active(G)) {  // NEXT-2: requests and answers as peer stores, no host round trip
-    Rank& rk = G.ranks[0];
-    CKR(launch_req_build(g, rk, s));
-    CKR(launch_req_push(g, rk, s));
-    CKR(launch_popc_scan(rk.req, rk.off_req, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
-    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, false, G.d_xerr, s));
-    CKR(launch_popc_scan(rk.reqin, rk.off_in, (uint64_t)C * W, rk.scan_tmp, rk.scan_tmp_bytes, s));
-    CKR(launch_resp_push(g, rk, s));
-    CKR(launch_xbarrier(G.xsig, G.d_sig_peers, G.world_size, G.world_rank, G.d_epoch, G.infos, false, G.d_xerr, s));
-    return BFS_OK;
-  }
+  // NEXT-2 peer exchange: nothing to do -- every K4 stored the candidates of other columns' rows
+  // in their owners' answer slots during the search (kernels.cu k_parent), and the last level's
+  // barrier made them visible; k_finalize reads them directly
+  if (peer_active(G)) return BFS_OK;
   for (Rank& rk : G.ranks) CKR(launch_req_build(g, rk, s));
   // requests: rank (i,j) sends req segment c to (i,c), which stores it as reqin segment j
   if (G.world_size == 1) {
@@ -953,7 +941,8 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
     par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : nullptr;  // no parent: not computed
-    CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr, s));
+    CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr,
+                        peer_active(G), s));
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[2], s));
   for (size_t k = 0; k < nl; ++k) {

@@ -1634,7 +1634,9 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
                                                                const uint32_t* __restrict__ inv_col,
                                                                LevelInfo* info, uint32_t hot_words, int R,
                                                                uint64_t Wc, int blog,
-                                                               uint32_t* const* __restrict__ fold_dst, int fused) {
+                                                               uint32_t* const* __restrict__ fold_dst, int fused,
+                                                               uint32_t* const* __restrict__ pred_dst, int jcol,
+                                                               uint64_t block) {
   extern __shared__ __align__(16) unsigned char psmem[];
   uint32_t (*queue)[1024] = reinterpret_cast<uint32_t (*)[1024]>(psmem);
   uint32_t* s_hot = reinterpret_cast<uint32_t*>(psmem) + (kParentThreads / 32) * 1024;
@@ -1643,7 +1645,22 @@ __global__ void __launch_bounds__(kParentThreads, 1) k_parent(uint32_t* vis, con
   // parent candidate of local row r.  (Measured: the owned rows' candidates interleaved with
   // their levels, so k_finalize gathers one 8-byte record per vertex: finalize -0.03 ms but the
   // stride-2 writes of K4 and K2 +0.1 ms per BFS at s26 -- partial sectors; not kept.)
-  auto put_pred = [&](uint64_t r, uint32_t val) { pred[r] = val; };
+  // With the peer exchange (C > 1) the candidate of a row of another column block c goes
+  // straight into the owner's answer slot for this column (pred_dst[c] = respin of P_ic +
+  // jcol*block, indexed by the owned offset): the owner's finalize then reads the winner
+  // column's candidate there, and no end-of-search request/answer round runs.  A stale candidate
+  // (this column reaching the row at a later level than the winner) lands in a slot the owner
+  // never reads: the winner is the lowest column that reached the row at its first level.
+  auto put_pred = [&](uint64_t r, uint32_t val) {
+    if (pred_dst) {
+      const uint64_t c = blog >= 0 ? (r >> blog) : r / block;
+      if ((int)c != jcol) {
+        pred_dst[c][r - c * block] = val;
+        return;
+      }
+    }
+    pred[r] = val;
+  };
   unsigned ndisc = 0;
   // P2: frontier bits of the hot (relabeled, highest-degree) column prefix of each of the R
   // column segments, so most frontier tests of the CSR scans stay in shared memory
@@ -1877,16 +1894,19 @@ cudaError_t launch_parent(const Geom& g, Rank& rk, bool fused, bool force_ptr64,
   if (hw > g.words_block()) hw = g.words_block();
   if (blog < 0) hw = 0;
   const size_t smem = (size_t)(kParentThreads / 32) * 1024 * 4 + (size_t)(g.R * hw > 4 ? g.R * hw : 4) * 4;
+  // peer exchange: fold bitmaps and the parent candidates of other columns' rows as peer stores
+  uint32_t* const* fold = g.C > 1 ? rk.fold_dst : nullptr;
+  uint32_t* const* pdst = fold ? rk.respin_dst : nullptr;
   if (rk.csr_ptr32 && !force_ptr64)
     k_parent<uint32_t><<<(unsigned)grid, kParentThreads, smem, s>>>(
         rk.vis, rk.vold, nwords, rk.csr_ptr32, rk.csr_col, rk.all_front, rk.pred, rk.pmin,
-        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog,
-        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
+        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog, fold,
+        fused ? 1 : 0, pdst, rk.j, g.block);
   else
     k_parent<ull><<<(unsigned)grid, kParentThreads, smem, s>>>(
         rk.vis, rk.vold, nwords, rk.csr_ptr, rk.csr_col, rk.all_front, rk.pred, rk.pmin,
-        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog,
-        g.C > 1 ? rk.fold_dst : nullptr, fused ? 1 : 0);
+        g.C > 1 ? rk.sendbuf : nullptr, rk.inv_col, rk.info, (uint32_t)hw, g.R, g.words_block(), blog, fold,
+        fused ? 1 : 0, pdst, rk.j, g.block);
   return cudaGetLastError();
 }
 
@@ -2079,6 +2099,7 @@ struct FinalizeArgs {
   const uint32_t* req;      // [C*W] request bitmaps
   const uint32_t* off_req;  // exclusive popcount scan of req
   const uint32_t* respin;   // answers, segment c at c*block
+  int direct;               // peer exchange: respin[c*block + p] is column c's candidate (pushed by K4)
   int j;
   uint64_t block, W;
 };
@@ -2100,6 +2121,8 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
       const int c = a.winner ? (int)a.winner[p] : a.j;
       if (c == a.j) {
         v = (int64_t)a.pred_own[p];
+      } else if (a.direct) {
+        v = (int64_t)a.respin[(uint64_t)c * a.block + p];
       } else {
         const uint64_t wi = (uint64_t)c * a.W + (p >> 5);
         const uint32_t below = a.req[wi] & ((1u << (p & 31)) - 1u);
@@ -2118,8 +2141,10 @@ __global__ void k_finalize(FinalizeArgs a, int64_t* parent_out, int32_t* level_o
   if (level_out) *reinterpret_cast<int4*>(level_out + t0) = make_int4(l[0], l[1], l[2], l[3]);
 }
 
-cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s) {
+cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, bool direct,
+                            cudaStream_t s) {
   FinalizeArgs a;
+  a.direct = direct ? 1 : 0;
   a.vis_own = rk.vis + (uint64_t)rk.j * g.words_block();
   a.level = rk.level;
   a.pred_own = rk.pred + (uint64_t)rk.j * g.block;
@@ -2239,48 +2264,6 @@ cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Peer exchange of the resolution (no host round trip): the requester stores its request segment
-// c into P_ic's reqin (segment j); the responder stores each answer straight into the
-// requester's respin at the position the requester computes from its own request bitmap.
-__global__ void k_req_push(const uint32_t* req, uint32_t* const* __restrict__ dst, uint64_t W, int C) {
-  for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < W * (uint64_t)C;
-       gid += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t c = gid / W;
-    if (dst[c]) dst[c][gid - c * W] = req[gid];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();
-}
-
-cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s) {
-  const uint64_t n = g.words_block() * g.C;
-  const uint64_t blocks = (n + 255) / 256, cap = (uint64_t)g.nsm * 8;
-  k_req_push<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(rk.req, rk.reqin_dst, g.words_block(), g.C);
-  return cudaGetLastError();
-}
-
-// the packed answers of segment c (count from the request scan) copied to P_ic in 16-B stores
-__global__ void k_resp_copy(const uint32_t* resp, const uint32_t* off, uint32_t* const* __restrict__ dst, uint64_t W,
-                            uint64_t block, int C, int j) {
-  for (int c = 0; c < C; ++c) {
-    if (c == j || !dst[c]) continue;
-    const uint64_t n = off[(uint64_t)(c + 1) * W] - off[(uint64_t)c * W];
-    const uint4* src = reinterpret_cast<const uint4*>(resp + (uint64_t)c * block);
-    uint4* d = reinterpret_cast<uint4*>(dst[c]);
-    const uint64_t n4 = (n + 3) / 4;  // block is a multiple of 4: the padded tail stays in range
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * blockDim.x)
-      d[t] = src[t];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();
-}
-
-cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s) {
-  cudaError_t e = launch_resp_pack(g, rk, s);  // packed locally (coalesced), then one bulk copy per peer
-  if (e != cudaSuccess) return e;
-  k_resp_copy<<<g.nsm * 4, 256, 0, s>>>(rk.resp, rk.off_in, rk.respin_dst, g.words_block(), g.block, g.C, rk.j);
-  return cudaGetLastError();
-}
 
 // ------------------------------------------------------------------ m_comp, degree
 __global__ void __launch_bounds__(256) k_mcomp(const uint32_t* vis_own, const uint32_t* tdeg, const uint32_t* fwd_own,

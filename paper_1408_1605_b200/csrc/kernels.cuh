@@ -38,7 +38,8 @@ cudaError_t launch_level_end(LevelCtrl* ctrl, const LevelInfo* infos, int nlocal
                              cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s);
 
 // Finalize: parent/level outputs for owned vertices whose parent is local.
-cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, cudaStream_t s);
+cudaError_t launch_finalize(const Geom& g, Rank& rk, int64_t* parent_out, int32_t* level_out, bool direct,
+                            cudaStream_t s);
 
 // Parent resolution (C > 1): build request bitmaps and answer requests (k_finalize reads them).
 cudaError_t launch_req_build(const Geom& g, Rank& rk, cudaStream_t s);
@@ -47,8 +48,6 @@ cudaError_t launch_popc_scan(const uint32_t* bits, uint32_t* off, uint64_t nword
 size_t popc_scan_tmp_bytes(uint64_t nwords);
 cudaError_t launch_resp_pack(const Geom& g, Rank& rk, cudaStream_t s);
 // peer exchange variants (stores into the peers' reqin / respin through rk.reqin_dst / respin_dst)
-cudaError_t launch_req_push(const Geom& g, Rank& rk, cudaStream_t s);
-cudaError_t launch_resp_push(const Geom& g, Rank& rk, cudaStream_t s);
 
 cudaError_t launch_seg_totals(const uint32_t* off, uint64_t W, int C, unsigned long long* totals, cudaStream_t s);
 
