@@ -181,6 +181,20 @@ int bfs_degree(bfs_graph* g, uint64_t v, uint64_t* degree);
  * Returns after the outputs are complete (the stream is synchronised). */
 int bfs_run(bfs_graph* g, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats);
 
+/* n BFS back to back (the Graph500 loop over sampled roots): root k = roots[k]
+ * (host array) writes its outputs to parent[k] / level[k], each an array like bfs_run's (host
+ * or device; parent / level themselves may be NULL, or any entry NULL, to skip that output).
+ * With host outputs, root k's device-to-host copies run on a second stream while root k+1
+ * searches (two device staging buffers per local rank, allocated on the first such batch; the
+ * copies only overlap if the host buffers are page-locked, e.g. cudaHostRegister / pinned).
+ * Entries may repeat a buffer: its contents are then those of the last root written to it.
+ * stats: NULL or an array of n records.  Returns after every output is complete; on an error
+ * the outputs of the failing root and any later root are undefined.  BFS_ERANGE if any root >=
+ * nverts (nothing run), BFS_EINVAL if n < 0 or roots is NULL with n > 0.  Every rank passes the
+ * same roots (COLLECTIVE like bfs_run). */
+int bfs_run_batch(bfs_graph* g, const uint64_t* roots, int n, int64_t* const* parent, int32_t* const* level,
+                  bfs_stats* stats);
+
 /* m_comp of the last run: number of input tuples whose source was reached, duplicates and
  * self-loops included (the TEPS numerator).  Summed over all ranks. */
 int bfs_mcomp(bfs_graph* g, uint64_t* m_comp);

@@ -59,6 +59,7 @@ class LevelRecord(ctypes.Structure):
 
 
 EXPORTS = ["bfs_nccl_unique_id", "bfs_graph_create", "bfs_graph_info", "bfs_set_opts", "bfs_degree", "bfs_run",
+           "bfs_run_batch",
            "bfs_mcomp", "bfs_level_times", "bfs_gather", "bfs_load_edges", "bfs_free_edges", "bfs_destroy",
            "bfs_strerror", "bfs_last_error"]
 DEBUG_POS64 = 1
@@ -83,6 +84,8 @@ def lib(build: bool = False):
         L.bfs_set_opts.argtypes = [p, ctypes.POINTER(Opts)]
         L.bfs_degree.argtypes = [p, u64, ctypes.POINTER(u64)]
         L.bfs_run.argtypes = [p, u64, p, p, ctypes.POINTER(Stats)]
+        L.bfs_run_batch.argtypes = [p, ctypes.POINTER(u64), i, ctypes.POINTER(p), ctypes.POINTER(p),
+                                    ctypes.POINTER(Stats)]
         L.bfs_mcomp.argtypes = [p, ctypes.POINTER(u64)]
         L.bfs_level_times.argtypes = [p, ctypes.POINTER(LevelRecord), i, ctypes.POINTER(i)]
         L.bfs_gather.argtypes = [p, p, p, p, p]
@@ -212,6 +215,24 @@ class Graph:
         _check(lib().bfs_run(self._h, int(root), _ptr(parent), _ptr(level),
                              ctypes.byref(st) if want_stats else None))
         return st
+
+    def run_batch(self, roots, parents=None, levels=None, want_stats=False):
+        """bfs_run_batch: one BFS per root, outputs into parents[k] / levels[k] (lists of buffers, host
+        or device; None to skip). Host copies of root k overlap root k+1's search (pinned buffers).
+        Returns the per-root Stats when want_stats."""
+        n = len(roots)
+        r = (ctypes.c_uint64 * max(n, 1))(*[int(x) for x in roots])
+
+        def ptrs(bufs):
+            if bufs is None:
+                return None
+            if len(bufs) != n:
+                raise ValueError("one output buffer (or None) per root")
+            return (ctypes.c_void_p * max(n, 1))(*[_ptr(b) for b in bufs])
+
+        st = (Stats * max(n, 1))() if want_stats else None
+        _check(lib().bfs_run_batch(self._h, r, n, ptrs(parents), ptrs(levels), st))
+        return [st[k] for k in range(n)] if want_stats else None
 
     def bfs(self, root: int):
         """Convenience: (level int32[nout], parent int64[nout]) as host numpy arrays."""

@@ -114,6 +114,8 @@ struct Rank {
   LevelInfo* info = nullptr;             // [1]
   int64_t* parent_tmp = nullptr;         // [block] parent staging for host outputs / resolution
   int32_t* level_tmp = nullptr;          // [block] level staging for host outputs
+  int64_t* parent_tmp2 = nullptr;        // bfs_run_batch: the second staging pair (odd roots),
+  int32_t* level_tmp2 = nullptr;         //   allocated on the first batch with host outputs
   // parent resolution (C>1)
   uint32_t* req = nullptr;       // [C * block/32] request bitmaps: rows whose parent lives at P_ic
   uint32_t* reqin = nullptr;     // [C * block/32] requests received from P_ic (rows of segment c)
@@ -185,6 +187,12 @@ struct Graph {
   unsigned long long* d_epoch = nullptr;
   int* d_xerr = nullptr;
   std::vector<void*> ipc_opened;      // cudaIpcOpenMemHandle mappings to close
+  // bfs_run_batch: host copies of root k on copy_stream while root k+1 searches on `stream`;
+  // batch_slot = k & 1 selects the staging pair (-1 outside a batch)
+  int batch_slot = -1;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t fin_ev[2] = {nullptr, nullptr};   // finalize of the slot's root done (on stream)
+  cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the slot's host copies done (on copy_stream)
 };
 
 }  // namespace bfs200

@@ -251,6 +251,16 @@ static void release_graph(Graph* G) {
   G->ev.clear();
   for (cudaEvent_t e : G->tail_ev) cudaEventDestroy(e);
   G->tail_ev.clear();
+  if (G->copy_stream) {
+    cudaStreamSynchronize(G->copy_stream);
+    cudaStreamDestroy(G->copy_stream);
+    G->copy_stream = nullptr;
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (G->fin_ev[k]) cudaEventDestroy(G->fin_ev[k]);
+    if (G->copy_ev[k]) cudaEventDestroy(G->copy_ev[k]);
+    G->fin_ev[k] = G->copy_ev[k] = nullptr;
+  }
   drop_graph(*G);
   if (G->h_infos) cudaFreeHost(G->h_infos);
   if (G->h_ctrl) cudaFreeHost(G->h_ctrl);
@@ -852,6 +862,23 @@ static int build_level_graph(Graph& G) {
   return BFS_OK;
 }
 
+// bfs_run_batch resources, created on the first batch with host outputs: the second staging pair
+// of every local rank, the copy stream and the slot events
+static int batch_setup(Graph& G) {
+  if (G.copy_stream) return BFS_OK;
+  int rc;
+  for (Rank& rk : G.ranks) {
+    if ((rc = G_alloc(G, (void**)&rk.parent_tmp2, G.g.block * 8))) return rc;
+    if ((rc = G_alloc(G, (void**)&rk.level_tmp2, G.g.block * 4))) return rc;
+  }
+  for (int k = 0; k < 2; ++k) {
+    CKR(cudaEventCreateWithFlags(&G.fin_ev[k], cudaEventDisableTiming));
+    CKR(cudaEventCreateWithFlags(&G.copy_ev[k], cudaEventDisableTiming));
+  }
+  CKR(cudaStreamCreateWithFlags(&G.copy_stream, cudaStreamNonBlocking));
+  return BFS_OK;
+}
+
 static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_stats* stats) {
   const Geom& g = G.g;
   cudaStream_t s = G.stream;
@@ -938,20 +965,40 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
     if ((rc = resolve_parents(G))) return rc;
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[1], s));
+  // bfs_run_batch: staging pair of this root's slot, free once the copies of root k-2 are done;
+  // the host copies then run on the copy stream, overlapping the next root's search
+  const int slot = G.batch_slot;
+  const bool staged = (parent && !par_is_dev) || (level && !lev_is_dev);
+  const bool async_copy = slot >= 0 && staged;
+  if (async_copy) {
+    if ((rc = batch_setup(G))) return rc;
+    CKR(cudaStreamWaitEvent(s, G.copy_ev[slot], 0));
+  }
   for (size_t k = 0; k < nl; ++k) {
     Rank& rk = G.ranks[k];
-    par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : rk.parent_tmp) : nullptr;  // no parent: not computed
-    CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : rk.level_tmp) : nullptr,
+    int64_t* ptmp = slot == 1 ? rk.parent_tmp2 : rk.parent_tmp;
+    int32_t* ltmp = slot == 1 ? rk.level_tmp2 : rk.level_tmp;
+    par_dev[k] = parent ? (par_is_dev ? parent + k * g.block : ptmp) : nullptr;  // no parent: not computed
+    CKR(launch_finalize(g, rk, par_dev[k], level ? (lev_is_dev ? level + k * g.block : ltmp) : nullptr,
                         peer_active(G), s));
   }
   if (G.opts.phase_timing) CKR(cudaEventRecord(G.tail_ev[2], s));
-  for (size_t k = 0; k < nl; ++k) {
-    Rank& rk = G.ranks[k];
-    if (parent && !par_is_dev)
-      CKR(cudaMemcpyAsync(parent + k * g.block, rk.parent_tmp, g.block * 8, cudaMemcpyDefault, s));
-    if (level && !lev_is_dev)
-      CKR(cudaMemcpyAsync(level + k * g.block, rk.level_tmp, g.block * 4, cudaMemcpyDefault, s));
-  }
+  // host copies of the staged outputs: on the stream (bfs_run), or on the copy stream once this
+  // run's small statistics reads are done (bfs_run_batch; a D2H copy engine serves its queue in
+  // order, so a statistics read queued behind this root's 0.5 GB copy would hold the host until
+  // the copy ends and nothing would overlap)
+  auto host_copies = [&](cudaStream_t cs) -> int {
+    for (size_t k = 0; k < nl; ++k) {
+      Rank& rk = G.ranks[k];
+      if (parent && !par_is_dev)
+        CKR(cudaMemcpyAsync(parent + k * g.block, par_dev[k], g.block * 8, cudaMemcpyDefault, cs));
+      if (level && !lev_is_dev)
+        CKR(cudaMemcpyAsync(level + k * g.block, slot == 1 ? rk.level_tmp2 : rk.level_tmp, g.block * 4,
+                            cudaMemcpyDefault, cs));
+    }
+    return BFS_OK;
+  };
+  if (!async_copy && (rc = host_copies(s))) return rc;
   CKR(cudaStreamSynchronize(s));
   if (peer_active(G)) {  // the resolution's barriers
     int xerr = 0;
@@ -1000,6 +1047,12 @@ static int run(Graph& G, uint64_t root, int64_t* parent, int32_t* level, bfs_sta
         (owner_local ? 1 : 0) + 1 + nlev + nl * ((fused_of(G) ? 6ull : 7ull) * nlev + 1) + ((g.C > 1 && parent) ? nl * (peer ? 6 : 4) : 0) +
         G.xlaunches +
         (peer ? 2ull * nlev + ((G.ranks[0].j == owner_j && !owner_local) ? 1 : 0) : 0);
+  }
+  if (async_copy) {  // after the statistics reads: root k's copies overlap root k+1's search
+    CKR(cudaEventRecord(G.fin_ev[slot], s));
+    CKR(cudaStreamWaitEvent(G.copy_stream, G.fin_ev[slot], 0));
+    if ((rc = host_copies(G.copy_stream))) return rc;
+    CKR(cudaEventRecord(G.copy_ev[slot], G.copy_stream));
   }
   return BFS_OK;
 }
@@ -1130,6 +1183,31 @@ int bfs_run(bfs_graph* gp, uint64_t root, int64_t* parent, int32_t* level, bfs_s
   } catch (std::bad_alloc&) {
     return set_err(BFS_ENOMEM, "host allocation failed");
   }
+}
+
+int bfs_run_batch(bfs_graph* gp, const uint64_t* roots, int n, int64_t* const* parent, int32_t* const* level,
+                  bfs_stats* stats) {
+  ENTER(gp);
+  NvtxRange r_run("bfs200: bfs_run_batch");
+  if (n < 0 || (n > 0 && !roots)) return set_err(BFS_EINVAL, "bad roots / n");
+  for (int k = 0; k < n; ++k)
+    if (roots[k] >= G.g.nverts)
+      return set_err(BFS_ERANGE, "roots[%d] = %llu >= nverts %llu", k, (ull)roots[k], (ull)G.g.nverts);
+  int rc = BFS_OK;
+  try {
+    for (int k = 0; k < n && rc == BFS_OK; ++k) {
+      G.batch_slot = k & 1;
+      rc = run(G, roots[k], parent ? parent[k] : nullptr, level ? level[k] : nullptr, stats ? stats + k : nullptr);
+    }
+  } catch (std::bad_alloc&) {
+    rc = set_err(BFS_ENOMEM, "host allocation failed");
+  }
+  G.batch_slot = -1;
+  if (G.copy_stream) {  // every host output complete
+    const cudaError_t e = cudaStreamSynchronize(G.copy_stream);
+    if (e != cudaSuccess && rc == BFS_OK) rc = cuda_fail(G, e, "bfs_run_batch: host copies", __FILE__, __LINE__);
+  }
+  return rc;
 }
 
 int bfs_mcomp(bfs_graph* gp, uint64_t* m_comp) {

@@ -421,3 +421,47 @@ def test_unaligned_device_outputs(bfs):
     pd, ld = pbuf[1:], lbuf[1:]  # 8- and 4-byte offsets
     g.run(r, pd, ld)
     assert np.array_equal(ld.cpu().numpy()[:n], ol) and np.array_equal(pd.cpu().numpy()[:n], op)
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 2)])
+def test_run_batch(bfs, grid):
+    """bfs_run_batch: every root's outputs equal the oracle's, for pinned and pageable host buffers
+    (the copies of root k overlap root k+1's search), device buffers, a host buffer reused by
+    several roots (it ends with the last one), a NULL entry, and per-root stats."""
+    scale = 14
+    s, d = inputs.generate(scale)
+    n = 1 << scale
+    og = oracle.Graph(n, s, d)
+    g = make_graph(bfs, s, d, n, *grid)
+    roots = [int(r) for r in inputs.sample_roots(n, 5, inputs.nonisolated_mask(n, s, d))]
+    exp = [og.bfs(r) for r in roots]
+    nout = g.info.nout
+    pin = [torch.empty(nout, dtype=torch.int64).pin_memory() for _ in roots]
+    lpin = [torch.empty(nout, dtype=torch.int32).pin_memory() for _ in roots]
+    page = [np.empty(nout, dtype=np.int64) for _ in roots]
+    dev = [torch.empty(nout, dtype=torch.int64, device="cuda") for _ in roots]
+    for bufs, lbufs in ((pin, lpin), (page, None), (dev, None)):
+        st = g.run_batch(roots, bufs, lbufs, want_stats=True)
+        for k, (ol, op) in enumerate(exp):
+            pa = bufs[k].cpu().numpy() if hasattr(bufs[k], "cpu") else bufs[k]
+            assert np.array_equal(pa[:n], op), f"parent mismatch root {roots[k]}"
+            assert (pa[n:] == -1).all()
+            if lbufs is not None:
+                assert np.array_equal(lbufs[k].numpy()[:n], ol), f"level mismatch root {roots[k]}"
+            assert st[k].nlevels == int(ol.max()) + 1
+    # one host buffer for every root: it holds the last root's tree; a NULL entry skips a root's output
+    shared = torch.empty(nout, dtype=torch.int64).pin_memory()
+    g.run_batch(roots, [shared] * len(roots))
+    assert np.array_equal(shared.numpy()[:n], exp[-1][1])
+    page2 = [np.full(nout, 7, dtype=np.int64) for _ in roots]
+    bufs = list(page2)
+    bufs[1] = None
+    g.run_batch(roots, bufs)
+    assert (page2[1] == 7).all() and np.array_equal(page2[2][:n], exp[2][1])
+    # a single bfs_run after a batch still sees its own staging
+    ph = torch.empty(nout, dtype=torch.int64).pin_memory()
+    g.run(roots[0], ph)
+    assert np.array_equal(ph.numpy()[:n], exp[0][1])
+    with pytest.raises(bfs.BfsError) as e:
+        g.run_batch([roots[0], 1 << 40])
+    assert e.value.status == bfs.BFS_ERANGE
