@@ -73,9 +73,13 @@ def main():
     lall = np.empty(info.npad, dtype=np.int32) if rank == 0 else None
     ok, bad, checked = True, [], []
     og = None
+    batch_check = a.scale <= 20  # bfs_run_batch vs the single runs (rank-local outputs kept on the host)
+    single = []
     for r in roots:
         g.run(r, parent, level)  # the first root runs the host-driven loop, later roots the graph loop
         mc = g.mcomp()
+        if batch_check:
+            single.append((parent.cpu().numpy().copy(), level.cpu().numpy().copy()))
         g.gather(parent, level, pall, lall)
         if rank != 0:
             continue
@@ -98,11 +102,23 @@ def main():
                     and (lall[n:] == -1).all() and (pall[n:] == -1).all())
         if not good:
             bad.append(r)
+    batch_bad = []
+    if batch_check:  # the same roots through bfs_run_batch into pinned host buffers (copies overlap searches)
+        pb = [torch.empty(info.nout, dtype=torch.int64).pin_memory() for _ in roots]
+        lb = [torch.empty(info.nout, dtype=torch.int32).pin_memory() for _ in roots]
+        g.run_batch(roots, pb, lb)
+        batch_bad = [r for r, (sp, sl), p_, l_ in zip(roots, single, pb, lb)
+                     if not (np.array_equal(p_.numpy(), sp) and np.array_equal(l_.numpy(), sl))]
+        flag = torch.tensor([len(batch_bad)], device="cuda")
+        dist.all_reduce(flag)
+        if flag.item():
+            bad.append("run_batch")
     dist.barrier()
     g.close()
     report = {"world": world, "grid": f"{R}x{C}", "scale": a.scale, "roots": len(roots), "block": int(info.block),
               "transport": "peer" if a.peer else "nccl", "exchange": a.exchange,
-              "check": "stream-validator V1-V6 + m_comp" if a.stream_validate else "bit-exact vs oracle"}
+              "check": "stream-validator V1-V6 + m_comp" if a.stream_validate else "bit-exact vs oracle",
+              "run_batch_checked": batch_check}
     if rank == 0:
         ok = not bad
         report.update({"ok": ok, "mismatched_roots": bad})
