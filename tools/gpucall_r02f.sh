@@ -1,18 +1,12 @@
-# K1 pipe A/B, full GPU tests (incl. SNAP), compute-sanitizer runs (1 GPU)
-mkdir -p gpurun_out/sanitizer
-python -c "
-import __graft_entry__ as g; g.build()
-from paper_1408_1605_b200 import _build
-for ns in (2, 4): _build.build_variant(f'pipe{ns}', [f'BFS200_K1PIPE={ns}'])
-" > gpurun_out/r2f_build.log 2>&1
-for v in default pipe2 pipe4; do
-  if [ $v = default ]; then L=""; else L=paper_1408_1605_b200/build/variants/lib$v.so; fi
-  BFS200_LIB=$L timeout 300 python tools/ab_expand.py --roots 8 >> gpurun_out/r2f_ab.log 2>&1
-done
-timeout 1500 python -m pytest tests -m gpu -x -q -rs > gpurun_out/r2f_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2f_tests.log
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_run.py > gpurun_out/sanitizer/r02_${tool}_s12.log 2>&1; echo "rc=$?" >> gpurun_out/sanitizer/r02_${tool}_s12.log
-done
-SAN_SCALE=18 timeout 1200 compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_run.py > gpurun_out/sanitizer/r02_racecheck_s18.log 2>&1; echo "rc=$?" >> gpurun_out/sanitizer/r02_racecheck_s18.log
-SAN_SCALE=18 timeout 1200 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_run.py > gpurun_out/sanitizer/r02_memcheck_s18.log 2>&1; echo "rc=$?" >> gpurun_out/sanitizer/r02_memcheck_s18.log
-cat gpurun_out/r2f_ab.log; tail -3 gpurun_out/r2f_tests.log; for f in gpurun_out/sanitizer/r02_*; do echo $f; tail -3 $f; done
+# 4 GPUs at HEAD: GPU tests, bench N=1 / 2 (1x2) / 4 (2x2, 4x1)
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2f4_build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -rs > gpurun_out/r2f4_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2f4_tests.log
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > gpurun_out/r2f4_bench1.log 2>&1; echo "rc=$?" >> gpurun_out/r2f4_bench1.log
+run() { n=$1; tag=$2; shift 2; timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29600 + RANDOM % 300)) bench.py --gpus $n --steps 20 --warmup 3 "$@" > gpurun_out/r2f4_bench_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/r2f4_bench_$tag.log; }
+CUDA_VISIBLE_DEVICES=0,1 run 2 1x2
+CUDA_VISIBLE_DEVICES=0,1 run 2 2x1 --grid 2x1
+run 4 2x2
+run 4 4x1 --grid 4x1
+for f in gpurun_out/r2f4_bench1.log gpurun_out/r2f4_bench_*.log; do grep '^{' $f | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$f', d['config']['grid'], round(d['value'],1), round(d['ms_per_step'],3), d['roofline']['frac'], json.dumps({k: round(v,3) for k,v in d.get('phase_ms_per_step',{}).items()}))"; done
