@@ -1030,10 +1030,13 @@ __device__ __noinline__ void long_tiles_p2(const uint32_t* __restrict__ row, con
 #pragma unroll
   for (int k = 0; k < AHEAD; ++k) rec_load(k, t0 + (uint32_t)(NS + k) * stride);
   const uint32_t ahead = (uint32_t)(AHEAD + NS) * stride;
-  for (uint32_t t = t0;;) {
+  // The exit test breaks out of the loop instead of returning from inside it: a RET waits for
+  // every load in flight (the caller may read any register), so a predicated RET at the top of
+  // each phase made every phase wait for the rows and records prefetched for the next ones.
+  for (uint32_t t = t0; t < nA;) {
 #pragma unroll
     for (int p = 0; p < NS; ++p) {
-      if (t >= nA) return;  // warp-uniform
+      if (t >= nA) break;  // warp-uniform
       const int sr = (p + AHEAD) % NS;  // slot of tile q+AHEAD (its record is loaded)
       rows_issue(sr);
       rec_load(sr, t + ahead);  // overflow past 2^32 cannot reach back below nA: nA + ahead < 2^32
@@ -1205,6 +1208,7 @@ __device__ __noinline__ void short_tiles_p2(const uint32_t* __restrict__ row, co
   cols_load(0);
   cols_load(1);
   rows_issue(0, t0);
+  // (leaving by break as in long_tiles_p2 costs this loop registers: 32-64 B of spills, slower)
   for (uint32_t t = t0;;) {
 #pragma unroll
     for (int p = 0; p < NS; ++p) {
