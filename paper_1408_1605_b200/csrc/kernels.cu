@@ -41,7 +41,7 @@ typedef unsigned long long ull;
 #endif
 // row slots of the pipelined long-tile loop of K1 (long_tiles_p2; 0 = the double-buffered loop)
 #ifndef BFS200_K1PIPE
-#define BFS200_K1PIPE 3
+#define BFS200_K1PIPE 4
 #endif
 
 // ------------------------------------------------------------------ small helpers
