@@ -29,19 +29,21 @@ namespace bfs200 {
 
 typedef unsigned long long ull;
 
-// the pipelined short-tile loop of K1 in P2 levels (short_tiles_p2; 0 = the staged loop)
-#ifndef BFS200_K1AHEAD  // long_tiles_p2: tiles whose rows are in flight ahead of the one tested
-#define BFS200_K1AHEAD (BFS200_K1PIPE - 1)
-#endif
 #ifndef BFS200_EMIT_SMEM  // K3 emit pass: dense chunks' column offsets staged by async copies
 #define BFS200_EMIT_SMEM 1
 #endif
+// the pipelined short-tile loop of K1 in P2 levels (short_tiles_p2; 0 = the staged loop)
 #ifndef BFS200_SHORTPIPE
 #define BFS200_SHORTPIPE 1
 #endif
-// row slots of the pipelined long-tile loop of K1 (long_tiles_p2; 0 = the double-buffered loop)
+// row slots of the pipelined long-tile loop of K1 (long_tiles_p2; 0 = the double-buffered loop):
+// one row segment (1 x C = 1 graphs, SEG1) / several (C > 1: the probe's segment lookup costs
+// registers; measured on a loopback 1x2 at s26: 3 slots 2.79 ms, 4 slots 2.88 ms per peak level)
 #ifndef BFS200_K1PIPE
 #define BFS200_K1PIPE 4
+#endif
+#ifndef BFS200_K1PIPE_SEGS
+#define BFS200_K1PIPE_SEGS 3
 #endif
 
 // ------------------------------------------------------------------ small helpers
@@ -1321,7 +1323,8 @@ __device__ __forceinline__ void expand_body(const uint32_t* __restrict__ row, co
     };
     ull t = (ull)blockIdx.x * WARPS + wid;
     if constexpr (!P1 && BFS200_K1PIPE > 0 && E <= 8) {
-      long_tiles_p2<E, SEG1, POS32, BFS200_K1PIPE, BFS200_K1AHEAD>(
+      constexpr int NS = SEG1 ? BFS200_K1PIPE : BFS200_K1PIPE_SEGS;
+      long_tiles_p2<E, SEG1, POS32, NS, NS - 1>(
           row, tileA, (uint32_t)nA, (uint32_t)t, (uint32_t)stride, vis, hw, sa, bl, bmask, lane, info);
     } else {
     uint4 rec = t < nA ? tileA[t] : make_uint4(0, 0, 0, 0);

@@ -67,6 +67,7 @@ def test_strerror_and_null_args(L):
     assert L.bfs_strerror(-2) == b"vertex id out of range"
     # null graph handles are rejected before touching the GPU
     assert L.bfs_run(None, 0, None, None, None) == bfs.BFS_EINVAL
+    assert L.bfs_run_batch(None, None, 0, None, None, None) == bfs.BFS_EINVAL
     assert L.bfs_mcomp(None, None) == bfs.BFS_EINVAL
     assert L.bfs_graph_create(None, None, 0, 0, 1, 1, None, None, None) == bfs.BFS_EINVAL
     L.bfs_destroy(None)  # NULL-safe
